@@ -1,0 +1,180 @@
+/*
+ * bgp.h -- C ABI of the B200-native bigGP likelihood path (libbgp.so).
+ *
+ * The reference (blockgp 0.1.0, pure Python) has no native library: its hot
+ * path is a set of registered worker operations dispatched through
+ * `Cluster.run(op_id, **kwargs)` (bg/transport/base.py:229-234) whose
+ * arithmetic lives in numpy/scipy -> OpenBLAS/LAPACK.  Each entry point below
+ * replaces one of those operations (or the BLAS/LAPACK calls inside it); the
+ * citation after each declaration names the reference code it stands in
+ * for.  `bg/` = /root/reference/pkg/src/blockgp/.
+ *
+ * Conventions
+ *  - All matrices are FP64.  Every pointer marked (device) is a CUDA device
+ *    pointer allocated and owned by the caller; the library never frees
+ *    caller memory and only uses scratch it owns inside the context.
+ *  - Triangular objects (n x n, lower) are stored as PACKED TILES: T = ceil(n/b)
+ *    tile rows, tiles (I, J) with I >= J stored column-major over the tile
+ *    grid at index  J*T - J*(J-1)/2 + (I-J)  (0-based), each tile b x b
+ *    column-major.  The padded tail carries the identity on the diagonal and
+ *    zeros elsewhere; the strict upper triangle of diagonal tiles is zero
+ *    (bg/distla/objects.py:1-9, 60-80).
+ *  - Rectangular objects (n x m) are stored TRANSPOSED as m x n tiles
+ *    (Tm = ceil(m/b) tile rows, Tn = ceil(n/b) tile columns, tile (I, J) at
+ *    index J*Tm + I, column-major inside), zero padded.  The transpose makes
+ *    the left triangular solve L X = B a right solve X^T L^T = B^T, which runs
+ *    on the same panel kernels as the Cholesky.
+ *  - Vectors are dense, length T*b, zero padded.
+ *  - `stream` is a cudaStream_t.  Calls are stream-ordered and asynchronous
+ *    unless they return a host scalar or a status that depends on device
+ *    data (bgp_potrf, bgp_logdet, bgp_sumsq, bgp_trsv, bgp_trsm_rect), which
+ *    synchronize the stream before returning.
+ *  - Return value: BGP_OK (0) or a negative BGP_E* code; device-data
+ *    conditions are reported through `info` out-parameters.
+ *  - A context is bound to one CUDA device and is not re-entrant
+ *    (bg/transport/base.py:1-7: one master thread, one operation at a time).
+ */
+#ifndef BGP_H
+#define BGP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BGP_OK 0
+#define BGP_E_CUDA (-1)        /* CUDA runtime / driver failure           */
+#define BGP_E_ARG (-2)         /* invalid argument or nonconforming shape  */
+#define BGP_E_UNSUPPORTED (-3) /* generator / smoothness not built in      */
+
+/* object kinds (bg/grid.py:198-234 "triangular" | "rectangular" | "vector") */
+#define BGP_TRI 0
+#define BGP_RECT 1
+#define BGP_VEC 2
+
+/* generator families (bg/gp/kernels.py:49-180) */
+#define BGP_GEN_ZERO 0          /* gen.zero                         :49-53  */
+#define BGP_GEN_DELTA 1         /* gen.delta                        :56-59  */
+#define BGP_GEN_LINEAR_INDEX 2  /* gen.linear_index (params[0] = n) :62-65  */
+#define BGP_GEN_MATERN 3        /* gen.matern[-nugget].*            :68-111 */
+#define BGP_GEN_SQEXP 4         /* gen.sqexp[-nugget].*             :68-109 */
+#define BGP_GEN_WHITE 5         /* gen.white.*                      :151-172 */
+#define BGP_GEN_PRODUCT 6       /* gen.matern-product-nugget.*      :114-148 */
+
+/* generator parts (bg/gp/kernels.py:77-93) */
+#define BGP_PART_COV 0      /* coords x coords, nugget on i == j (if on) */
+#define BGP_PART_CROSS 1    /* coords x pred_coords, no nugget           */
+#define BGP_PART_PRED 2     /* pred_coords x pred_coords, no nugget      */
+#define BGP_PART_PREDVAR 3  /* vector, params[0]                         */
+
+typedef struct bgp_ctx* bgp_ctx_t;
+
+/* Generator description.  Replaces the registry lookup of a generator id
+ * (bg/registry.py:24-28) with a fixed device menu; unknown ids are rejected
+ * on the host (no CPU fallback). */
+typedef struct {
+  int family;          /* BGP_GEN_*                                          */
+  int part;            /* BGP_PART_*                                         */
+  int nugget;          /* 1: add params[nparams-1] where global i == j (cov)  */
+  int nparams;
+  double params[8];    /* theta as in bg/gp/kernels.py:109-111, 174-180       */
+  double nu;           /* Matern smoothness 0.5 / 1.5 / 2.5 (nu1 for product)  */
+  double nu2;          /* second-axis smoothness (product kernel)             */
+} bgp_generator;
+
+/* ---- context ------------------------------------------------------------ */
+int bgp_init(int device, bgp_ctx_t* ctx);
+int bgp_finalize(bgp_ctx_t ctx);
+const char* bgp_last_error(bgp_ctx_t ctx);
+/* library build string (arch, version) for provenance */
+const char* bgp_version(void);
+/* number of kernels this context has launched (evidence counter) */
+int64_t bgp_launch_count(bgp_ctx_t ctx);
+
+/* ---- K1 covariance construction ------------------------------------------
+ * replaces distla.construct (bg/distla/kernels.py:35-75) + pad_block
+ * (bg/distla/objects.py:60-80) + the gen.* generators (bg/gp/kernels.py).
+ * X: (device) nx x dim row-major coordinates, Y: (device) ny x dim (may be
+ * NULL unless part is CROSS/PRED).  kind BGP_TRI: out = packed tiles of the
+ * nx x nx lower triangle; BGP_RECT: out = transposed tiles of nx x ny
+ * (i.e. tiles of the ny x nx matrix); BGP_VEC: out = length ceil(nx/b)*b. */
+int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
+                  const double* X, int64_t nx, const double* Y, int64_t ny,
+                  int dim, int tile, double* out, void* stream);
+
+/* ---- K2 tiled Cholesky ----------------------------------------------------
+ * replaces distla.cholesky / _cholesky_sweep (bg/distla/kernels.py:110-194),
+ * in place on packed tiles.  info = 0 on success, else the 1-based global
+ * row of the first non-positive pivot (LAPACK potrf convention); the caller
+ * maps it to NotPositiveDefinite(block) with its layout (kernels.py:146-148). */
+int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile,
+              int64_t* info, void* stream);
+
+/* ---- K3 solves -------------------------------------------------------------
+ * bgp_trsv replaces distla.solve_vector (bg/distla/kernels.py:200-250):
+ * x <- L^{-1} x (trans = 0, "forward") or L^{-T} x (trans = 1, "back").
+ * bgp_trsm_rect replaces distla.solve_rect (kernels.py:253-307) on a
+ * transposed rectangular object B^T (m x n tiles), in place.
+ * info = 0, or the 1-based global row of the first zero diagonal entry
+ * (SingularDiagonal, kernels.py:245-246, 302-303). */
+int bgp_trsv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x,
+             int trans, int64_t* info, void* stream);
+int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+                  double* Bt, int64_t m, int trans, int64_t* info, void* stream);
+
+/* ---- K3 crossproducts (bg/distla/kernels.py:387-487) -----------------------
+ * Vt: transposed rectangular object (m x n tiles). */
+int bgp_xprod_mat_vec(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
+                      int tile, const double* u, double* w, void* stream);
+int bgp_xprod_self_diag(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
+                        int tile, double* d, void* stream);
+int bgp_xprod_self(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
+                   int tile, double* S, void* stream);
+
+/* ---- K3d reductions (bg/distla/kernels.py:493-522, __init__.py:154-162) ----
+ * logdet = 2 sum_{i<n} log L_ii (fixed-order tree sum); info = 1-based row
+ * of the first non-positive diagonal (SingularDiagonal) or 0. */
+int bgp_logdet(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+               double* out, int64_t* info, void* stream);
+int bgp_sumsq(bgp_ctx_t ctx, const double* x, int64_t n, double* out,
+              void* stream);
+
+/* ---- plumbing: distribute / collect / remote_apply("sub") -------------------
+ * bgp_pack replaces distla.split (kernels.py:538-544, objects.py:83-105):
+ * dense row-major (device) nrow x ncol array with leading dimension ld ->
+ * tiles of `kind` (the lower triangle only for BGP_TRI; for BGP_RECT the
+ * dense array is the n x m matrix and the tiles hold its transpose).
+ * bgp_unpack is the inverse (bg/distla/objects.py:108-123, assemble);
+ * triangular unpack writes the lower triangle and zeros above it.
+ * bgp_tri_diagonal extracts diag (collect_diagonal, __init__.py:141-151).
+ * bgp_sub: out = a - b elementwise over `count` doubles (kernels.py:564). */
+int bgp_pack(bgp_ctx_t ctx, int kind, const double* dense, int64_t nrow,
+             int64_t ncol, int64_t ld, int tile, double* tiles, void* stream);
+int bgp_unpack(bgp_ctx_t ctx, int kind, const double* tiles, int64_t nrow,
+               int64_t ncol, int tile, double* dense, int64_t ld, void* stream);
+int bgp_tri_diagonal(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+                     double* d, void* stream);
+int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out,
+            int64_t count, void* stream);
+
+/* ---- tile-level primitives (multi-GPU driver, look-ahead schedules) -------
+ * bgp_tile_potrf: factor one b x b diagonal tile in place (info as above,
+ *   `row0` = 0-based global row of the tile for the info value).
+ * bgp_panel_trsm: X <- A L_d^{-T} for `count` b x b tiles at A (stride
+ *   b*b doubles), L_d one factored diagonal tile (kernels.py:163-164).
+ * bgp_tile_update: C -= A B^T over a list of `count` (C, A, B) tile index
+ *   triples into three packed-tile bases (kernels.py:188-192); a triple with
+ *   lower != 0 updates only the lower triangle (diagonal SYRK). */
+int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0,
+                   int64_t* info, void* stream);
+int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count,
+                   int tile, void* stream);
+int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
+                    const double* Bbase, const int32_t* triples /*device, 4 per*/,
+                    int64_t count, int tile, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGP_H */

@@ -1,0 +1,92 @@
+// Internal host-side declarations shared by the libbgp translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/bgp.h"
+
+namespace bgp {
+
+// device-side generator description (built from bgp_generator on the host)
+struct GenDev {
+  int family, part, nugget, np;
+  double p[8];
+  double sqrt2nu, sqrt2nu2;
+  int nucode, nucode2;  // 0: nu=1/2, 1: 3/2, 2: 5/2
+  int dim;
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  int64_t launches = 0;
+  // device scratch owned by the context
+  unsigned long long* d_info = nullptr;  // [0]: potrf / trsv status
+  double* d_red = nullptr;               // reduction partials
+  size_t red_cap = 0;
+  double* d_dinv = nullptr;  // inverted 32x32 diagonal sub-blocks
+  size_t dinv_cap = 0;
+  double* d_part = nullptr;  // generic partial buffer (crossproducts)
+  size_t part_cap = 0;
+  int32_t* d_items = nullptr;
+  size_t items_cap = 0;
+  void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
+};
+
+int set_err(Ctx* ctx, const char* what, cudaError_t e);
+int check_launch(Ctx* ctx, const char* what);
+int ensure(Ctx* ctx, void** buf, size_t* cap, size_t bytes);
+
+// encode a 3-D FP64 tensor map over `ntiles` b x b column-major tiles:
+// dims (b rows, b cols, ntiles), box {box0 rows, box1 cols, 1}, 128B swizzle
+int make_tile_map(Ctx* ctx, CUtensorMap* map, const double* base, int b, int64_t ntiles, int box0,
+                  int box1, bool swizzle128);
+
+int construct(Ctx* ctx, int kind, const GenDev& g, const double* X, int64_t nx, const double* Y,
+              int64_t ny, int b, double* out, cudaStream_t s);
+
+// tile kernels
+int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s);
+int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
+int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
+                      int trans, cudaStream_t s);
+
+// DMMA/TMA GEMM problems
+enum GemmMode { GEMM_CHOL_TRAIL = 0, GEMM_RECT_TRAIL = 1, GEMM_SYRK_RECT = 2, GEMM_LIST = 3 };
+struct GemmProblem {
+  int mode;
+  int b;
+  int T;    // tile rows of the packed triangle (L or S)
+  int J;    // panel index (trailing modes)
+  int Tm;   // tile rows of a transposed rectangular object
+  int Tn;   // tile columns of a transposed rectangular object
+  int64_t count;  // GEMM_LIST: number of (C, A, B, lower) tuples
+  const int32_t* items;
+  double alpha, beta;  // D = beta*C + alpha*sum(A B^T)
+};
+int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
+                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s);
+
+int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s);
+int launch_trsm_rect_back(Ctx* ctx, const double* L, int64_t n, int b, double* Bt, int64_t m,
+                          cudaStream_t s);
+int launch_logdet(Ctx* ctx, const double* L, int64_t n, int b, cudaStream_t s);
+int launch_sumsq(Ctx* ctx, const double* x, int64_t n, cudaStream_t s);
+int launch_rowdot(Ctx* ctx, const double* Vt, int64_t n, int64_t m, int b, const double* u, double* w,
+                  cudaStream_t s);
+int launch_pack(Ctx* ctx, int kind, const double* dense, int64_t nrow, int64_t ncol, int64_t ld, int b,
+                double* tiles, cudaStream_t s);
+int launch_unpack(Ctx* ctx, int kind, const double* tiles, int64_t nrow, int64_t ncol, int b,
+                  double* dense, int64_t ld, cudaStream_t s);
+int launch_tri_diagonal(Ctx* ctx, const double* L, int64_t n, int b, double* d, cudaStream_t s);
+int launch_sub(Ctx* ctx, const double* a, const double* bb, double* out, int64_t count, cudaStream_t s);
+
+}  // namespace bgp
+
+// the opaque C handle is the context itself
+struct bgp_ctx : public bgp::Ctx {};

@@ -1,0 +1,368 @@
+// extern "C" entry points of libbgp.so (declared in include/bgp.h) and the
+// host-side drivers that sequence the tile kernels.
+//
+// The Cholesky driver is the reference's right-looking block sweep
+// (bg/distla/kernels.py:139-194) with one GPU owning every tile: per panel J,
+// tile POTRF of (J,J), panel TRSM of tiles (I>J, J), then one persistent DMMA
+// launch for the whole trailing SYRK/GEMM.  All launches are stream-ordered;
+// the only host synchronization is the final status read.
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+
+#include "bgp_common.cuh"
+#include "bgp_internal.h"
+
+namespace bgp {
+
+int set_err(Ctx* ctx, const char* what, cudaError_t e) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  ctx->err = buf;
+  return BGP_E_CUDA;
+}
+
+int check_launch(Ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ctx, what, e);
+  return BGP_OK;
+}
+
+int ensure(Ctx* ctx, void** buf, size_t* cap, size_t bytes) {
+  if (*cap >= bytes && *buf) return BGP_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(buf, bytes);
+  if (e != cudaSuccess) return set_err(ctx, "scratch allocation", e);
+  *cap = bytes;
+  return BGP_OK;
+}
+
+int make_tile_map(Ctx* ctx, CUtensorMap* map, const double* base, int b, int64_t ntiles, int box0, int box1,
+                  bool swizzle128) {
+  auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx->encode_fn);
+  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)b, (cuuint64_t)ntiles};
+  cuuint64_t strides[2] = {(cuuint64_t)b * 8, (cuuint64_t)b * b * 8};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d) b=%d ntiles=%lld box=%dx%d", (int)r, b,
+             (long long)ntiles, box0, box1);
+    ctx->err = buf;
+    return BGP_E_CUDA;
+  }
+  return BGP_OK;
+}
+
+static int read_info(Ctx* ctx, cudaStream_t s, int64_t* info) {
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpyAsync(&h, ctx->d_info, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(ctx, "status read", e);
+  if (info) *info = (int64_t)h;
+  return BGP_OK;
+}
+
+static int reset_info(Ctx* ctx, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(ctx->d_info, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return set_err(ctx, "status reset", e);
+  return BGP_OK;
+}
+
+static bool valid_tile(int b) { return b >= 128 && b <= 512 && (b % 128) == 0; }
+
+static int to_gendev(Ctx* ctx, const bgp_generator* g, int dim, GenDev* out) {
+  GenDev d{};
+  d.family = g->family;
+  d.part = g->part;
+  d.nugget = g->nugget;
+  d.np = g->nparams;
+  if (d.np < 0 || d.np > 8) {
+    ctx->err = "generator: nparams out of range";
+    return BGP_E_ARG;
+  }
+  for (int i = 0; i < 8; ++i) d.p[i] = g->params[i];
+  auto code = [](double nu) { return nu == 0.5 ? 0 : (nu == 1.5 ? 1 : (nu == 2.5 ? 2 : -1)); };
+  d.nucode = code(g->nu);
+  d.nucode2 = code(g->nu2);
+  // numpy evaluates np.sqrt(2.0 * nu) in FP64; sqrt is correctly rounded in both
+  d.sqrt2nu = std::sqrt(2.0 * g->nu);
+  d.sqrt2nu2 = std::sqrt(2.0 * g->nu2);
+  d.dim = dim;
+  if ((g->family == BGP_GEN_MATERN || g->family == BGP_GEN_PRODUCT) && g->part != BGP_PART_PREDVAR &&
+      d.nucode < 0) {
+    ctx->err = "unsupported Matern smoothness";
+    return BGP_E_UNSUPPORTED;
+  }
+  if (g->family == BGP_GEN_PRODUCT && g->part != BGP_PART_PREDVAR && (d.nucode2 < 0 || dim != 2)) {
+    ctx->err = "product kernel needs 2-D coordinates and half-integer smoothness";
+    return BGP_E_UNSUPPORTED;
+  }
+  if (dim < 1 || dim > 4) {
+    ctx->err = "coordinate dimension must be 1..4";
+    return BGP_E_ARG;
+  }
+  if (g->family < BGP_GEN_ZERO || g->family > BGP_GEN_PRODUCT) {
+    ctx->err = "unknown generator family";
+    return BGP_E_UNSUPPORTED;
+  }
+  *out = d;
+  return BGP_OK;
+}
+
+}  // namespace bgp
+
+using namespace bgp;
+
+extern "C" {
+
+const char* bgp_version(void) { return "libbgp 0.1 sm_100a (FP64 DMMA + TMA)"; }
+
+int bgp_init(int device, bgp_ctx_t* out) {
+  bgp_ctx* ctx = new bgp_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_info, 64);
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_info, 0, 64);
+  if (e == cudaSuccess) {
+    ctx->red_cap = 1024 * sizeof(double);
+    e = cudaMalloc(&ctx->d_red, ctx->red_cap);
+  }
+  if (e == cudaSuccess) {
+    cudaDriverEntryPointQueryResult q;
+    e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ctx->encode_fn, cudaEnableDefault, &q);
+    if (e == cudaSuccess && q != cudaDriverEntryPointSuccess) e = cudaErrorNotSupported;
+  }
+  if (e != cudaSuccess) {
+    fprintf(stderr, "bgp_init: %s\n", cudaGetErrorString(e));
+    delete ctx;
+    *out = nullptr;
+    return BGP_E_CUDA;
+  }
+  *out = ctx;
+  return BGP_OK;
+}
+
+int bgp_finalize(bgp_ctx_t ctx) {
+  if (!ctx) return BGP_OK;
+  cudaSetDevice(ctx->device);
+  cudaFree(ctx->d_info);
+  cudaFree(ctx->d_red);
+  if (ctx->d_dinv) cudaFree(ctx->d_dinv);
+  if (ctx->d_part) cudaFree(ctx->d_part);
+  if (ctx->d_items) cudaFree(ctx->d_items);
+  delete ctx;
+  return BGP_OK;
+}
+
+const char* bgp_last_error(bgp_ctx_t ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t bgp_launch_count(bgp_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen, const double* X, int64_t nx, const double* Y,
+                  int64_t ny, int dim, int tile, double* out, void* stream) {
+  if (!valid_tile(tile) || nx < 1 || (kind == BGP_RECT && ny < 1)) return BGP_E_ARG;
+  GenDev g;
+  int rc = to_gendev(ctx, gen, dim, &g);
+  if (rc) return rc;
+  return construct(ctx, kind, g, X, nx, Y, ny, tile, out, (cudaStream_t)stream);
+}
+
+int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int b = tile;
+  const int T = (int)((n + b - 1) / b);
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  const size_t dinv_bytes = (size_t)(b / 32) * 32 * 32 * sizeof(double);
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
+  const int64_t ntiles = tri_count(T);
+  const int64_t tsz = (int64_t)b * b;
+  for (int J = 0; J < T; ++J) {
+    double* djj = tiles + tri_index(J, J, T) * tsz;
+    if ((rc = launch_tile_potrf(ctx, djj, b, (int64_t)J * b, ctx->d_dinv, s))) return rc;
+    if (J + 1 < T) {
+      double* panel = tiles + tri_index(J + 1, J, T) * tsz;
+      if ((rc = launch_panel_trsm(ctx, djj, ctx->d_dinv, panel, T - J - 1, b, 0, s))) return rc;
+      GemmProblem p{};
+      p.mode = GEMM_CHOL_TRAIL;
+      p.b = b;
+      p.T = T;
+      p.J = J;
+      p.alpha = -1.0;
+      p.beta = 1.0;
+      if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
+    }
+  }
+  return read_info(ctx, s, info);
+}
+
+int bgp_trsv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x, int trans, int64_t* info,
+             void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  if ((rc = launch_trsv(ctx, L, n, tile, x, trans, s))) return rc;
+  return read_info(ctx, s, info);
+}
+
+int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* Bt, int64_t m, int trans,
+                  int64_t* info, void* stream) {
+  if (!valid_tile(tile) || n < 1 || m < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int b = tile;
+  const int T = (int)((n + b - 1) / b), Tm = (int)((m + b - 1) / b);
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  if (trans) {
+    if ((rc = launch_trsm_rect_back(ctx, L, n, b, Bt, m, s))) return rc;
+    return read_info(ctx, s, info);
+  }
+  const size_t per_tile = (size_t)(b / 32) * 32 * 32;
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, per_tile * T * sizeof(double)))) return rc;
+  if ((rc = launch_diag_inv(ctx, L, T, b, n, ctx->d_dinv, s))) return rc;
+  const int64_t tsz = (int64_t)b * b;
+  const int64_t nL = tri_count(T), nV = (int64_t)Tm * T;
+  for (int J = 0; J < T; ++J) {
+    const double* ljj = L + tri_index(J, J, T) * tsz;
+    if ((rc = launch_panel_trsm(ctx, ljj, ctx->d_dinv + per_tile * J, Bt + (int64_t)J * Tm * tsz, Tm, b, 0, s)))
+      return rc;
+    if (J + 1 < T) {
+      GemmProblem p{};
+      p.mode = GEMM_RECT_TRAIL;
+      p.b = b;
+      p.T = T;
+      p.J = J;
+      p.Tm = Tm;
+      p.Tn = T;
+      p.alpha = -1.0;
+      p.beta = 1.0;
+      if ((rc = launch_gemm(ctx, p, Bt, Bt, nV, L, nL, nV, s))) return rc;
+    }
+  }
+  return read_info(ctx, s, info);
+}
+
+int bgp_xprod_mat_vec(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m, int tile, const double* u, double* w,
+                      void* stream) {
+  if (!valid_tile(tile) || !u) return BGP_E_ARG;
+  return launch_rowdot(ctx, Vt, n, m, tile, u, w, (cudaStream_t)stream);
+}
+
+int bgp_xprod_self_diag(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m, int tile, double* d, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  return launch_rowdot(ctx, Vt, n, m, tile, nullptr, d, (cudaStream_t)stream);
+}
+
+int bgp_xprod_self(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m, int tile, double* S, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  const int b = tile;
+  const int Tn = (int)((n + b - 1) / b), Tm = (int)((m + b - 1) / b);
+  GemmProblem p{};
+  p.mode = GEMM_SYRK_RECT;
+  p.b = b;
+  p.Tm = Tm;
+  p.Tn = Tn;
+  p.alpha = 1.0;
+  p.beta = 0.0;
+  const int64_t nV = (int64_t)Tm * Tn;
+  int rc = reset_info(ctx, (cudaStream_t)stream);
+  if (rc) return rc;
+  return launch_gemm(ctx, p, S, Vt, nV, Vt, nV, tri_count(Tm), (cudaStream_t)stream);
+}
+
+int bgp_logdet(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* out, int64_t* info, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  if ((rc = launch_logdet(ctx, L, n, tile, s))) return rc;
+  cudaError_t e = cudaMemcpyAsync(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return set_err(ctx, "logdet copy", e);
+  return read_info(ctx, s, info);
+}
+
+int bgp_sumsq(bgp_ctx_t ctx, const double* x, int64_t n, double* out, void* stream) {
+  if (n < 0) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_sumsq(ctx, x, n, s);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(ctx, "sumsq copy", e);
+  return BGP_OK;
+}
+
+int bgp_pack(bgp_ctx_t ctx, int kind, const double* dense, int64_t nrow, int64_t ncol, int64_t ld, int tile,
+             double* tiles, void* stream) {
+  if (!valid_tile(tile) || nrow < 1) return BGP_E_ARG;
+  return launch_pack(ctx, kind, dense, nrow, ncol, ld, tile, tiles, (cudaStream_t)stream);
+}
+
+int bgp_unpack(bgp_ctx_t ctx, int kind, const double* tiles, int64_t nrow, int64_t ncol, int tile, double* dense,
+               int64_t ld, void* stream) {
+  if (!valid_tile(tile) || nrow < 1) return BGP_E_ARG;
+  return launch_unpack(ctx, kind, tiles, nrow, ncol, tile, dense, ld, (cudaStream_t)stream);
+}
+
+int bgp_tri_diagonal(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* d, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  return launch_tri_diagonal(ctx, L, n, tile, d, (cudaStream_t)stream);
+}
+
+int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out, int64_t count, void* stream) {
+  return launch_sub(ctx, a, b, out, count, (cudaStream_t)stream);
+}
+
+int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0, int64_t* info, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
+  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s))) return rc;
+  return read_info(ctx, s, info);
+}
+
+int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, int tile, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t per_tile = (size_t)(tile / 32) * 32 * 32;
+  int rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, per_tile * sizeof(double));
+  if (rc) return rc;
+  // the diagonal tile passed here is a standalone factored tile: invert its
+  // 32x32 diagonal blocks (T = 1 packed triangle)
+  if ((rc = launch_diag_inv(ctx, Ld, 1, tile, tile, ctx->d_dinv, s))) return rc;
+  return launch_panel_trsm(ctx, Ld, ctx->d_dinv, A, count, tile, 0, s);
+}
+
+int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase, const int32_t* triples,
+                    int64_t count, int tile, void* stream) {
+  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
+  if (count == 0) return BGP_OK;
+  GemmProblem p{};
+  p.mode = GEMM_LIST;
+  p.b = tile;
+  p.count = count;
+  p.items = triples;
+  p.alpha = -1.0;
+  p.beta = 1.0;
+  // tensor-map extents: the caller's bases are only addressed through the
+  // listed indices; a generous bound keeps the maps valid
+  const int64_t big = (int64_t)1 << 30;
+  return launch_gemm(ctx, p, Cbase, Abase, big, Bbase, big, big, (cudaStream_t)stream);
+}
+
+}  // extern "C"

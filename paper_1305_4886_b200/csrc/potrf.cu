@@ -1,0 +1,292 @@
+// K2a tile POTRF, K2b panel TRSM and the 32x32 diagonal-block inverses.
+//
+// Replaces the LAPACK calls inside the reference's block sweep:
+//   la.cholesky(A_JJ)                       bg/distla/kernels.py:146-148
+//   solve_triangular(L_JJ, A_IJ^T)^T        bg/distla/kernels.py:163-164
+// and the diagonal TRSM inside solve_rect (kernels.py:304-306).
+//
+// tile_potrf: one CTA factors a b x b diagonal tile held in global memory
+// (it is L2-resident: the trailing update just wrote it).  Right-looking with
+// 32-wide sub-panels: warp 0 factors the 32x32 diagonal block in registers
+// (lane = row, shuffles), warp 1 inverts it, all threads apply the inverse to
+// the sub-panel below, and the in-tile trailing update runs on FP64 DMMA with
+// both operands in shared memory.  The first non-positive (or NaN) pivot
+// records its 1-based global row in *info and stops the factorization.
+//
+// panel_trsm: X = A L^{-T} for a column of b x b tiles.  One CTA owns a
+// 32-row slab of one tile in shared memory and sweeps the 32-wide column
+// blocks: X_k = S_k Dinv_k^T, then S_{>k} -= X_k L_{>k,k}^T.
+#include "bgp_common.cuh"
+#include "bgp_internal.h"
+
+namespace bgp {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NB = 32;        // sub-panel width
+constexpr int PLD = 36;       // smem leading dimension of the panel copy (conflict-free DMMA frags)
+constexpr int POTRF_THREADS = 256;
+
+// inverse of a lower-triangular 32x32 block held in smem D (ld 33);
+// lane = column of the inverse.  Writes Dinv_s (ld 33) and optionally global
+// (column-major 32x32).
+__device__ __forceinline__ void warp_trinv32(const double* D, double* Dinv_s, double* gout, int lane) {
+  double x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(D[i * 33 + k], x[k], s);
+    const double dii = D[i * 33 + i];
+    x[i] = (i == lane) ? 1.0 / dii : ((i > lane) ? -s / dii : 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    Dinv_s[i * 33 + lane] = x[i];
+    if (gout) gout[lane * NB + i] = x[i];
+  }
+}
+
+__global__ void __launch_bounds__(POTRF_THREADS, 1)
+    tile_potrf_kernel(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
+                      unsigned long long* __restrict__ info) {
+  extern __shared__ double sm[];
+  double* D = sm;                // 32 x 33
+  double* Dinv_s = D + NB * 33;  // 32 x 33
+  double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (*(volatile unsigned long long*)info != 0ull) return;  // an earlier step failed
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  const int nbk = b / NB;
+  for (int kb = 0; kb < nbk; ++kb) {
+    const int c0 = kb * NB;
+    // (1) factor the 32x32 diagonal block (rows/cols c0..c0+31)
+    if (warp == 0) {
+      double a[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a[j] = (j <= lane) ? A[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
+      int failj = -1;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (failj < 0) {
+          const double piv = __shfl_sync(FULL, a[j], j);
+          if (!(piv > 0.0)) {
+            failj = j;
+          } else {
+            const double ljj = sqrt(piv);
+            const double rinv = 1.0 / ljj;
+            a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
+#pragma unroll
+            for (int c = j + 1; c < NB; ++c) {
+              const double lcj = __shfl_sync(FULL, a[j], c);
+              if (lane >= c) a[c] = fma(-a[j], lcj, a[c]);
+            }
+          }
+        }
+      }
+      if (failj >= 0) {
+        if (lane == 0) {
+          set_info(info, row0 + c0 + failj + 1);
+          s_fail = 1;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          D[lane * 33 + j] = (j <= lane) ? a[j] : 0.0;
+          if (j <= lane) A[(int64_t)(c0 + j) * b + c0 + lane] = a[j];
+        }
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;
+    // (1b) invert it (warp 0); the inverse feeds the sub-panel solve and the
+    // panel TRSM kernel (global copy)
+    if (warp == 0) warp_trinv32(D, Dinv_s, dinv ? dinv + (int64_t)kb * NB * NB : nullptr, lane);
+    __syncthreads();
+    const int rest = b - c0 - NB;  // rows below the diagonal block
+    if (rest <= 0) break;
+    // (2) sub-panel X = A[c0+32:, c0:c0+32] Dinv^T  (in place + smem copy)
+    for (int r = tid; r < rest; r += POTRF_THREADS) {
+      const int64_t gi = c0 + NB + r;
+      double av[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) av[k] = A[(int64_t)(c0 + k) * b + gi];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k <= j; ++k) s = fma(av[k], Dinv_s[j * 33 + k], s);
+        A[(int64_t)(c0 + j) * b + gi] = s;
+        P[r * PLD + j] = s;
+      }
+    }
+    __syncthreads();
+    // (3) in-tile trailing update: A[i][j] -= sum_k X[i][k] X[j][k], rows/cols
+    // >= c0+32, lower triangle only, 8x8 DMMA blocks
+    const int nb8 = rest / 8;
+    const int nblk = nb8 * (nb8 + 1) / 2;
+    const int q = lane >> 2, s4 = lane & 3;
+    for (int blk = warp; blk < nblk; blk += POTRF_THREADS / 32) {
+      // decode blk -> (ib >= jb), row-major over the lower triangle
+      int ib = (int)((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
+      while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+      while (ib * (ib + 1) / 2 > blk) --ib;
+      const int jb = blk - ib * (ib + 1) / 2;
+      const int64_t gr = c0 + NB + ib * 8 + q;
+      const int64_t gc = c0 + NB + jb * 8 + 2 * s4;
+      double c0v = A[gc * b + gr], c1v = A[(gc + 1) * b + gr];
+#pragma unroll
+      for (int kk = 0; kk < NB / 4; ++kk) {
+        const double av = -P[(ib * 8 + q) * PLD + kk * 4 + s4];
+        const double bv = P[(jb * 8 + q) * PLD + kk * 4 + s4];
+        dmma884(c0v, c1v, av, bv);
+      }
+      if (ib != jb || gr >= gc) A[gc * b + gr] = c0v;
+      if (ib != jb || gr >= gc + 1) A[(gc + 1) * b + gr] = c1v;
+    }
+    __syncthreads();
+  }
+}
+
+// inverses of the 32x32 diagonal sub-blocks of every diagonal tile of a packed
+// triangle; zero diagonal -> info (SingularDiagonal, kernels.py:245-246)
+__global__ void diag_inv_kernel(const double* __restrict__ L, int T, int b, int64_t n,
+                                double* __restrict__ dinv, unsigned long long* __restrict__ info) {
+  __shared__ double D[NB * 33];
+  __shared__ double Dinv_s[NB * 33];
+  const int nbk = b / NB;
+  const int J = blockIdx.x / nbk, kb = blockIdx.x % nbk;
+  const int lane = threadIdx.x;
+  const double* tile = L + tri_index(J, J, T) * (int64_t)b * b;
+  const int c0 = kb * NB;
+#pragma unroll 4
+  for (int j = 0; j < NB; ++j)
+    D[lane * 33 + j] = (j <= lane) ? tile[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
+  __syncwarp();
+  const int64_t grow = (int64_t)J * b + c0 + lane;
+  const bool zero = (D[lane * 33 + lane] == 0.0) && grow < n;
+  const unsigned z = __ballot_sync(FULL, zero);
+  if (z) {
+    if (lane == 0) set_info(info, (int64_t)J * b + c0 + __ffs(z));
+    return;
+  }
+  warp_trinv32(D, Dinv_s, dinv + ((int64_t)J * nbk + kb) * NB * NB, lane);
+}
+
+// X = A L^{-T} (trans = 0) for `count` consecutive b x b tiles.
+constexpr int TRSM_THREADS = 256;
+constexpr int TRSM_R = 32;     // slab rows
+constexpr int TRSM_CH = 64;    // staged L rows per update chunk
+
+__global__ void __launch_bounds__(TRSM_THREADS, 2)
+    panel_trsm_kernel(const double* __restrict__ Ld, const double* __restrict__ dinv,
+                      double* __restrict__ Abase, int b, const unsigned long long* __restrict__ info) {
+  extern __shared__ double sm[];
+  double* S = sm;                       // b cols x TRSM_R rows, S[c*R + r]
+  double* Lc = S + (int64_t)b * TRSM_R;   // TRSM_CH x 33
+  double* Di = Lc + TRSM_CH * 33;       // 32 x 33
+  if (info && *(volatile const unsigned long long*)info != 0ull) return;
+  const int slabs = b / TRSM_R;
+  const int64_t t = blockIdx.x / slabs;
+  const int r0 = (blockIdx.x % slabs) * TRSM_R;
+  double* A = Abase + t * (int64_t)b * b;
+  const int tid = threadIdx.x, r = tid & 31, cw = tid >> 5;
+  // load slab (coalesced: 32 consecutive rows per column)
+  for (int idx = tid; idx < b * TRSM_R; idx += TRSM_THREADS) {
+    const int c = idx / TRSM_R, rr = idx % TRSM_R;
+    S[idx] = A[(int64_t)c * b + r0 + rr];
+  }
+  const int nbk = b / NB;
+  for (int kb = 0; kb < nbk; ++kb) {
+    const int c0 = kb * NB;
+    // stage Dinv_k (column-major in global) as Di[j*33 + k] = Dinv[j][k]
+    for (int idx = tid; idx < NB * NB; idx += TRSM_THREADS) {
+      const int col = idx / NB, row = idx % NB;
+      Di[row * 33 + col] = dinv[(int64_t)kb * NB * NB + idx];
+    }
+    __syncthreads();
+    // X_k = S_k Dinv^T : thread (r, cw) computes columns j = cw + 8u
+    double sv[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) sv[k] = S[(c0 + k) * TRSM_R + r];
+    double xo[NB / 8];
+#pragma unroll
+    for (int u = 0; u < NB / 8; ++u) {
+      const int j = cw + 8 * u;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) s = (k <= j) ? fma(sv[k], Di[j * 33 + k], s) : s;
+      xo[u] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < NB / 8; ++u) S[(c0 + cw + 8 * u) * TRSM_R + r] = xo[u];
+    __syncthreads();
+    // X row r into registers
+    double x[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) x[k] = S[(c0 + k) * TRSM_R + r];
+    // update remaining columns in chunks of TRSM_CH staged L rows
+    for (int cb = c0 + NB; cb < b; cb += TRSM_CH) {
+      __syncthreads();
+      for (int idx = tid; idx < TRSM_CH * NB; idx += TRSM_THREADS) {
+        const int k = idx / TRSM_CH, cc = idx % TRSM_CH;  // coalesced over cc
+        Lc[cc * 33 + k] = (cb + cc < b) ? Ld[(int64_t)(c0 + k) * b + cb + cc] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < TRSM_CH / 8; ++u) {
+        const int cc = cw + 8 * u;
+        const int c = cb + cc;
+        if (c < b) {
+          double s = S[c * TRSM_R + r];
+#pragma unroll
+          for (int k = 0; k < NB; ++k) s = fma(-x[k], Lc[cc * 33 + k], s);
+          S[c * TRSM_R + r] = s;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < b * TRSM_R; idx += TRSM_THREADS) {
+    const int c = idx / TRSM_R, rr = idx % TRSM_R;
+    A[(int64_t)c * b + r0 + rr] = S[idx];
+  }
+}
+
+int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s) {
+  const size_t smem = (size_t)(2 * NB * 33 + (b - NB) * PLD) * sizeof(double);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(tile_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done = true;
+  }
+  tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "tile_potrf");
+}
+
+int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s) {
+  diag_inv_kernel<<<T * (b / NB), 32, 0, s>>>(L, T, b, n, dinv, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "diag_inv");
+}
+
+int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
+                      int trans, cudaStream_t s) {
+  if (count <= 0) return BGP_OK;
+  (void)trans;
+  const size_t smem = ((size_t)b * TRSM_R + TRSM_CH * 33 + NB * 33) * sizeof(double);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done = true;
+  }
+  const int64_t grid = count * (b / TRSM_R);
+  panel_trsm_kernel<<<(unsigned)grid, TRSM_THREADS, smem, s>>>(Ld, dinv, A, b, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "panel_trsm");
+}
+
+}  // namespace bgp

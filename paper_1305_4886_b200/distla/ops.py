@@ -1,0 +1,370 @@
+"""Device implementations of the reference's distla operation ids.
+
+Each function here is registered under the same op id as the reference's
+worker SPMD function (bg/distla/kernels.py) and is invoked through
+`B200Cluster.run(op_id, **kwargs)` with the same keyword arguments.  The
+`ctx` argument is the cluster (the GPU is the worker).  All arithmetic is in
+libbgp (include/bgp.h); these functions allocate buffers, check shapes and
+map device status codes onto the reference's exceptions.
+"""
+
+import ctypes
+
+import numpy as np
+
+from .. import _lib, registry
+from ..errors import (DimensionMismatch, GeneratorError, NotPositiveDefinite,
+                      SingularDiagonal, UnknownFunction, UnsupportedSmoothness)
+from ..grid import BlockLayout
+from .objects import DevObj
+
+HALF_INTEGER_NU = (0.5, 1.5, 2.5)
+
+
+def _ntiles(n, b):
+    return -(-n // b)
+
+
+def _alloc(ctx, kind, n, m=None):
+    b = ctx.tile
+    T = _ntiles(n, b)
+    if kind == "triangular":
+        return ctx.empty((T * (T + 1) // 2, b, b))
+    if kind == "rectangular":
+        return ctx.empty((T * _ntiles(m, b), b, b))
+    return ctx.empty((T * b,))
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _need(ctx, name, kind):
+    obj = ctx.fetch(name)
+    if not isinstance(obj, DevObj) or obj.kind != kind:
+        raise DimensionMismatch(f"object {name!r} is not a device {kind} object")
+    return obj
+
+
+# ---------------------------------------------------------------------------
+# construction (bg/distla/kernels.py:35-75)
+
+def _device_generator(ctx, gen_id, params, inputs, kind):
+    g = registry.device_generator(gen_id)
+    params = np.asarray(params, dtype=float).ravel()
+    desc = _lib.Generator()
+    desc.family, desc.part, desc.nugget = g.family, g.part, int(g.nugget)
+    desc.nparams = len(params)
+    if len(params) > 8:
+        raise DimensionMismatch("at most 8 kernel parameters")
+    for i, v in enumerate(params):
+        desc.params[i] = float(v)
+    desc.nu = float(inputs.get("nu", inputs.get("nu1", 0.5))) if inputs else 0.5
+    desc.nu2 = float(inputs.get("nu2", 0.5)) if inputs else 0.5
+    fam = g.family
+    try:
+        if fam in (_lib.GEN_MATERN, _lib.GEN_SQEXP, _lib.GEN_PRODUCT) and g.part != _lib.PART_PREDVAR:
+            # the reference's generators raise inside the worker; those
+            # errors surface as GeneratorError (bg/distla/kernels.py:66-69)
+            if fam == _lib.GEN_PRODUCT:
+                nus = (desc.nu, desc.nu2)
+                rhos = params[1:3]
+            else:
+                nus = (desc.nu,) if fam == _lib.GEN_MATERN else ()
+                rhos = params[1:2]
+            for nu in nus:
+                if nu not in HALF_INTEGER_NU:
+                    raise UnsupportedSmoothness(
+                        f"nu={nu} not supported; use one of {HALF_INTEGER_NU}")
+            if fam == _lib.GEN_MATERN or fam == _lib.GEN_PRODUCT:
+                for rho in rhos:
+                    if rho <= 0:
+                        raise ValueError(f"range must be positive, got {rho}")
+        if fam == _lib.GEN_LINEAR_INDEX:
+            desc.params[0] = float(inputs["n"])
+            desc.nparams = 1
+    except Exception as exc:
+        raise GeneratorError(ctx.rank, exc) from exc
+    return g, desc
+
+
+@registry.register("distla.construct")
+def construct(ctx, name, kind, generator, params, inputs_name, row_layout, col_layout=None):
+    inputs = ctx.fetch(inputs_name) if inputs_name else {}
+    g, desc = _device_generator(ctx, generator, params, inputs, kind)
+    n = row_layout.n
+    m = col_layout.n if (kind == "rectangular" and col_layout is not None) else None
+    if kind == "rectangular" and col_layout is None:
+        raise DimensionMismatch("rectangular construction needs a column layout")
+    needs_points = g.family in (_lib.GEN_MATERN, _lib.GEN_SQEXP, _lib.GEN_PRODUCT) \
+        and g.part != _lib.PART_PREDVAR and kind != "vector"
+    X = Y = None
+    dim = 1
+    if needs_points:
+        key_x = "pred_coords" if g.part == _lib.PART_PRED else "coords"
+        X = ctx.device_input(inputs_name, key_x)
+        dim = X.shape[1]
+        if X.shape[0] < n:
+            raise GeneratorError(ctx.rank, IndexError(
+                f"{key_x} has {X.shape[0]} points, layout needs {n}"))
+        if g.part == _lib.PART_CROSS:
+            Y = ctx.device_input(inputs_name, "pred_coords")
+            if Y.shape[1] != dim or Y.shape[0] < m:
+                raise GeneratorError(ctx.rank, IndexError("pred_coords do not conform"))
+    out = _alloc(ctx, kind, n, m)
+    if name in ctx.store:
+        del ctx.store[name]
+    ctx.call("bgp_construct", _lib.KIND_CODE[kind], ctypes.byref(desc),
+             _ptr(X) if X is not None else None, n,
+             _ptr(Y) if Y is not None else None, m or 0, dim, ctx.tile, _ptr(out), ctx.stream)
+    cl = (col_layout or row_layout) if kind != "vector" else None
+    ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out)
+    ctx.log_event("construct")
+
+
+@registry.register("distla.split")
+def split(ctx, name, kind, array, row_layout, col_layout=None):
+    """Upload a master-side dense array (bg/distla/kernels.py:538-544)."""
+    a = np.asarray(array, dtype=float)
+    n = row_layout.n
+    if kind == "vector":
+        if a.shape != (n,):
+            raise DimensionMismatch(f"vector length {a.shape} != {n}")
+        m = None
+    elif kind == "triangular":
+        if a.shape != (n, n):
+            raise DimensionMismatch(f"triangular array {a.shape} != ({n}, {n})")
+        m = n
+    else:
+        if col_layout is None or a.shape != (n, col_layout.n):
+            raise DimensionMismatch("rectangular array does not match its layouts")
+        m = col_layout.n
+    dense = ctx.upload(a)
+    out = _alloc(ctx, kind, n, m)
+    ld = a.shape[1] if a.ndim == 2 else 1
+    ctx.call("bgp_pack", _lib.KIND_CODE[kind], _ptr(dense), n, m or 1, ld, ctx.tile,
+             _ptr(out), ctx.stream)
+    cl = (col_layout or row_layout) if kind != "vector" else None
+    ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out)
+
+
+# ---------------------------------------------------------------------------
+# Cholesky (bg/distla/kernels.py:110-194)
+
+@registry.register("distla.cholesky")
+def cholesky(ctx, name, out_name):
+    obj = _need(ctx, name, "triangular")
+    if out_name != name:
+        ctx.store[out_name] = obj
+        del ctx.store[name]
+    info = ctypes.c_int64(0)
+    try:
+        ctx.call("bgp_potrf", _ptr(obj.data), obj.n, obj.tile, ctypes.byref(info), ctx.stream)
+    except BaseException:
+        ctx.store.pop(out_name, None)  # no partial factor is retained
+        raise
+    if info.value:
+        ctx.store.pop(out_name, None)
+        raise NotPositiveDefinite((info.value - 1) // obj.row_layout.block_size + 1)
+    ctx.log_event("factor")
+    nt = obj.data.shape[0]
+    return {"peak_blocks": nt, "owned_blocks": nt, "tile": obj.tile}
+
+
+# ---------------------------------------------------------------------------
+# triangular solves (bg/distla/kernels.py:200-307)
+
+@registry.register("distla.solve_vector")
+def solve_vector(ctx, l_name, rhs_name, out_name, forward=True):
+    L = _need(ctx, l_name, "triangular")
+    rhs = _need(ctx, rhs_name, "vector")
+    if rhs.data.shape[0] != L.data.shape[1] * _ntiles(L.n, L.tile) or rhs.n != L.n:
+        raise DimensionMismatch("rhs does not conform to L")
+    x = rhs.data.clone()
+    info = ctypes.c_int64(0)
+    ctx.call("bgp_trsv", _ptr(L.data), L.n, L.tile, _ptr(x), 0 if forward else 1,
+             ctypes.byref(info), ctx.stream)
+    if info.value:
+        raise SingularDiagonal(f"zero diagonal at row {info.value}")
+    ctx.store[out_name] = DevObj("vector", rhs.row_layout, None, rhs.tile, x)
+    ctx.log_event("solve")
+
+
+@registry.register("distla.solve_rect")
+def solve_rect(ctx, l_name, rhs_name, out_name, forward=True):
+    L = _need(ctx, l_name, "triangular")
+    B = _need(ctx, rhs_name, "rectangular")
+    if B.n != L.n:
+        raise DimensionMismatch("rhs rows do not conform to L")
+    X = B.data.clone()
+    info = ctypes.c_int64(0)
+    ctx.call("bgp_trsm_rect", _ptr(L.data), L.n, L.tile, _ptr(X), B.m, 0 if forward else 1,
+             ctypes.byref(info), ctx.stream)
+    if info.value:
+        raise SingularDiagonal(f"zero diagonal at row {info.value}")
+    ctx.store[out_name] = DevObj("rectangular", B.row_layout, B.col_layout, B.tile, X)
+    ctx.log_event("solve")
+
+
+# ---------------------------------------------------------------------------
+# crossproducts (bg/distla/kernels.py:387-487)
+
+@registry.register("distla.xprod_mat_vec")
+def xprod_mat_vec(ctx, v_name, u_name, out_name):
+    V = _need(ctx, v_name, "rectangular")
+    u = _need(ctx, u_name, "vector")
+    if u.n != V.n:
+        raise DimensionMismatch("u does not conform to V")
+    w = _alloc(ctx, "vector", V.m)
+    ctx.call("bgp_xprod_mat_vec", _ptr(V.data), V.n, V.m, V.tile, _ptr(u.data), _ptr(w), ctx.stream)
+    ctx.store[out_name] = DevObj("vector", V.col_layout, None, V.tile, w)
+
+
+@registry.register("distla.xprod_self")
+def xprod_self(ctx, v_name, out_name):
+    V = _need(ctx, v_name, "rectangular")
+    S = _alloc(ctx, "triangular", V.m)
+    ctx.call("bgp_xprod_self", _ptr(V.data), V.n, V.m, V.tile, _ptr(S), ctx.stream)
+    ctx.store[out_name] = DevObj("triangular", V.col_layout, V.col_layout, V.tile, S)
+
+
+@registry.register("distla.xprod_self_diag")
+def xprod_self_diag(ctx, v_name, out_name):
+    V = _need(ctx, v_name, "rectangular")
+    d = _alloc(ctx, "vector", V.m)
+    ctx.call("bgp_xprod_self_diag", _ptr(V.data), V.n, V.m, V.tile, _ptr(d), ctx.stream)
+    ctx.store[out_name] = DevObj("vector", V.col_layout, None, V.tile, d)
+
+
+# ---------------------------------------------------------------------------
+# reductions (bg/distla/kernels.py:493-522)
+
+@registry.register("distla.logdet")
+def logdet(ctx, l_name):
+    L = _need(ctx, l_name, "triangular")
+    out = ctypes.c_double(0.0)
+    info = ctypes.c_int64(0)
+    ctx.call("bgp_logdet", _ptr(L.data), L.n, L.tile, ctypes.byref(out), ctypes.byref(info),
+             ctx.stream)
+    if info.value:
+        raise SingularDiagonal(f"non-positive diagonal at row {info.value}")
+    return out.value
+
+
+@registry.register("distla.sumsq")
+def sumsq(ctx, name):
+    x = _need(ctx, name, "vector")
+    out = ctypes.c_double(0.0)
+    ctx.call("bgp_sumsq", _ptr(x.data), x.n, ctypes.byref(out), ctx.stream)
+    return out.value
+
+
+# ---------------------------------------------------------------------------
+# collection (bg/distla/kernels.py:525-535, objects.py:108-123)
+
+def dense_of(ctx, obj):
+    """Unpadded host array of a device object (lower-triangular for
+    triangular objects)."""
+    torch = __import__("torch")
+    if obj.kind == "vector":
+        return obj.data[:obj.n].cpu().numpy().copy()
+    n, m = obj.n, (obj.m if obj.kind == "rectangular" else obj.n)
+    dense = torch.zeros((n, m), dtype=torch.float64, device=obj.data.device)
+    ctx.call("bgp_unpack", _lib.KIND_CODE[obj.kind], _ptr(obj.data), n, m, obj.tile,
+             _ptr(dense), m, ctx.stream)
+    return dense.cpu().numpy()
+
+
+def diagonal_of(ctx, obj):
+    torch = __import__("torch")
+    d = torch.empty((obj.n,), dtype=torch.float64, device=obj.data.device)
+    ctx.call("bgp_tri_diagonal", _ptr(obj.data), obj.n, obj.tile, _ptr(d), ctx.stream)
+    return d.cpu().numpy()
+
+
+def _blocks_of(dense, kind, rl, cl, diagonal_only):
+    """Reference-format {(I, J): block} pieces of an unpadded dense array."""
+    if kind == "vector":
+        bs = rl.block_size
+        x = np.zeros(rl.padded_n)
+        x[:rl.n] = dense
+        return {J: x[(J - 1) * bs:J * bs].copy() for J in range(1, rl.B + 1)}
+    cl = cl or rl
+    bsr, bsc = rl.block_size, cl.block_size
+    A = np.zeros((rl.padded_n, cl.padded_n))
+    A[:rl.n, :cl.n] = dense
+    if kind == "triangular":
+        for t in range(rl.n, rl.padded_n):
+            A[t, t] = 1.0
+    out = {}
+    for J in range(1, cl.B + 1):
+        for I in range(J if kind == "triangular" else 1, rl.B + 1):
+            blk = A[(I - 1) * bsr:I * bsr, (J - 1) * bsc:J * bsc]
+            if diagonal_only:
+                if I == J:
+                    out[(I, J)] = np.diag(blk).copy()
+            else:
+                out[(I, J)] = blk.copy()
+    return out
+
+
+@registry.register("distla.collect")
+def collect_blocks(ctx, name, diagonal_only=False):
+    """Operator-level collect: pieces in the object's API layout."""
+    obj = ctx.fetch(name)
+    if not isinstance(obj, DevObj):
+        raise DimensionMismatch(f"{name!r} is not a distributed object")
+    return _blocks_of(dense_of(ctx, obj), obj.kind, obj.row_layout, obj.col_layout,
+                      diagonal_only)
+
+
+# ---------------------------------------------------------------------------
+# elementwise helpers used through remote_apply (bg/distla/kernels.py:550-564)
+
+def _conform(a, b):
+    if not (isinstance(a, DevObj) and isinstance(b, DevObj) and a.kind == b.kind
+            and a.data.shape == b.data.shape and a.tile == b.tile):
+        raise DimensionMismatch("local pieces do not align")
+
+
+def _sub(ctx, a, b):
+    _conform(a, b)
+    out = ctx.empty(a.data.shape)
+    ctx.call("bgp_sub", _ptr(a.data), _ptr(b.data), _ptr(out), a.data.numel(), ctx.stream)
+    return DevObj(a.kind, a.row_layout, a.col_layout, a.tile, out)
+
+
+def _negate(ctx, a):
+    zero = DevObj(a.kind, a.row_layout, a.col_layout, a.tile, ctx.zeros(a.data.shape))
+    return _sub(ctx, zero, a)
+
+
+def _add(ctx, a, b):
+    return _sub(ctx, a, _negate(ctx, b))
+
+
+_ELEMENTWISE = {"sub": _sub, "add": _add, "negate": _negate}
+
+
+@registry.register("core.apply")
+def apply(ctx, op_id, input_names, output_name):
+    fn = _ELEMENTWISE.get(op_id)
+    if fn is None:
+        registry.lookup(op_id)  # UnknownFunction for ids that do not exist at all
+        raise UnknownFunction(f"{op_id!r} has no device implementation")
+    ctx.store[output_name] = fn(ctx, *[ctx.fetch(n) for n in input_names])
+
+
+def _not_on_path(op):
+    def fn(ctx, **kwargs):
+        raise UnknownFunction(f"{op!r} is not implemented on the b200 backend yet "
+                              "(simulation is outside the likelihood path)")
+    return fn
+
+
+for _op in ("distla.rnorm", "distla.mult_vector", "distla.mult_rect"):
+    registry.register(_op, _not_on_path(_op))
+for _op in ("sub", "add", "negate"):
+    registry.register(_op, _op)
+
+__all__ = ["BlockLayout", "dense_of", "diagonal_of"]
