@@ -174,6 +174,17 @@ int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
                     const double* Bbase, const int32_t* triples /*device, 4 per*/,
                     int64_t count, int tile, void* stream);
 
+/* ---- measurement ----------------------------------------------------------
+ * When profiling is on, bgp_potrf brackets every launch with CUDA events on
+ * the caller's stream (no extra synchronization: they are read at the
+ * status sync the call already does).  bgp_profile_read returns and clears
+ *   out[0] potrf ms  out[1] trsm ms  out[2] gemm (trailing update) ms
+ *   out[3] gemm launches  out[4] gemm algorithmic flops (b^3 k^2 per launch)
+ *   out[5] potrf launches  out[6] trsm launches  out[7] factorizations
+ * (stands in for the reference's event log, bg/transport/base.py:121-123). */
+int bgp_set_profiling(bgp_ctx_t ctx, int on);
+int bgp_profile_read(bgp_ctx_t ctx, double* out8);
+
 #ifdef __cplusplus
 }
 #endif

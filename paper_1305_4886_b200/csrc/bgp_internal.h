@@ -36,6 +36,11 @@ struct Ctx {
   int32_t* d_items = nullptr;
   size_t items_cap = 0;
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
+  // profiling (bgp_set_profiling / bgp_profile_read)
+  bool profile = false;
+  cudaEvent_t* events = nullptr;
+  int events_cap = 0;
+  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 int set_err(Ctx* ctx, const char* what, cudaError_t e);

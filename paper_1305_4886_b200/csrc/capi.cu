@@ -160,6 +160,8 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_dinv) cudaFree(ctx->d_dinv);
   if (ctx->d_part) cudaFree(ctx->d_part);
   if (ctx->d_items) cudaFree(ctx->d_items);
+  for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
+  delete[] ctx->events;
   delete ctx;
   return BGP_OK;
 }
@@ -188,12 +190,28 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   const int64_t ntiles = tri_count(T);
   const int64_t tsz = (int64_t)b * b;
+  // profiling: event k brackets launch k (potrf, trsm, gemm per panel)
+  const int nev = 3 * T + 1;
+  if (ctx->profile && ctx->events_cap < nev) {
+    for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
+    delete[] ctx->events;
+    ctx->events = new cudaEvent_t[nev];
+    for (int i = 0; i < nev; ++i) cudaEventCreate(&ctx->events[i]);
+    ctx->events_cap = nev;
+  }
+  int ev = 0;
+  auto mark = [&]() {
+    if (ctx->profile) cudaEventRecord(ctx->events[ev++], s);
+  };
+  mark();
   for (int J = 0; J < T; ++J) {
     double* djj = tiles + tri_index(J, J, T) * tsz;
     if ((rc = launch_tile_potrf(ctx, djj, b, (int64_t)J * b, ctx->d_dinv, s))) return rc;
+    mark();
     if (J + 1 < T) {
       double* panel = tiles + tri_index(J + 1, J, T) * tsz;
       if ((rc = launch_panel_trsm(ctx, djj, ctx->d_dinv, panel, T - J - 1, b, 0, s))) return rc;
+      mark();
       GemmProblem p{};
       p.mode = GEMM_CHOL_TRAIL;
       p.b = b;
@@ -202,9 +220,48 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
       p.alpha = -1.0;
       p.beta = 1.0;
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
+      mark();
     }
   }
-  return read_info(ctx, s, info);
+  rc = read_info(ctx, s, info);
+  if (rc == BGP_OK && ctx->profile) {
+    // events: [0] start, then per panel potrf | trsm | gemm boundaries
+    int k = 0;
+    for (int J = 0; J < T; ++J) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
+      ctx->prof[0] += ms;
+      ctx->prof[5] += 1;
+      ++k;
+      if (J + 1 < T) {
+        cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
+        ctx->prof[1] += ms;
+        ctx->prof[6] += 1;
+        ++k;
+        cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
+        ctx->prof[2] += ms;
+        ctx->prof[3] += 1;
+        const double kk = (double)(T - J - 1);
+        ctx->prof[4] += (double)b * b * b * kk * kk;
+        ++k;
+      }
+    }
+    ctx->prof[7] += 1;
+  }
+  return rc;
+}
+
+int bgp_set_profiling(bgp_ctx_t ctx, int on) {
+  ctx->profile = (on != 0);
+  return BGP_OK;
+}
+
+int bgp_profile_read(bgp_ctx_t ctx, double* out8) {
+  for (int i = 0; i < 8; ++i) {
+    out8[i] = ctx->prof[i];
+    ctx->prof[i] = 0.0;
+  }
+  return BGP_OK;
 }
 
 int bgp_trsv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x, int trans, int64_t* info,
