@@ -25,48 +25,73 @@
 #include "bgp_common.cuh"
 #include "bgp_internal.h"
 
+#include <stdio.h>
+
 namespace bgp {
 
-constexpr int BM = 128, BN = 128, BK = 8, STAGES = 4;
-constexpr int MMA_WARPS = 8;
-constexpr int THREADS = (MMA_WARPS + 1) * 32;
-constexpr int WM = 64, WN = 32;
-constexpr int STAGE_A_BYTES = BM * BK * 8;  // 8 KB
-constexpr int STAGE_BYTES = 2 * STAGE_A_BYTES;
-constexpr int CBUF_BYTES = BM * BN * 8;  // 128 KB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
+// Tile configuration.  One CTA per SM, three warpgroups:
+//   WG0  producers: warp 0 feeds consumer group 0's ring, warp 1 group 1's
+//        (setmaxnreg.dec 40);
+//   WG1, WG2  consumers: 4 MMA warps each (2 x 2 warps of 64x32), each group
+//        owns a 128x64 output block at a time (setmaxnreg.inc 232).
+// The two consumer groups take alternate blocks of the CTA's static schedule
+// and run concurrently, so one group's epilogue overlaps the other group's
+// main loop and the DMMA pipe never drains between blocks.
+constexpr int BM = 128, BN = 64, BK = 8, STAGES = 4;
+constexpr int GROUPS = 2;
+constexpr int WARPS_M = 2, WARPS_N = 2;       // per consumer group
+constexpr int GROUP_WARPS = WARPS_M * WARPS_N;
+constexpr int THREADS = 128 * (GROUPS + 1);
+constexpr int WM = 64, WN = 32;                // warp tile
+constexpr int MI = WM / 8, NJ = WN / 8;        // 8x8 DMMA tiles per warp
+constexpr int STAGE_A_BYTES = BM * BK * 8;     // 8 KB: 8 boxes of 16x8
+constexpr int STAGE_B_BYTES = BN * BK * 8;     // 4 KB: 4 boxes of 16x8
+constexpr int STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
+constexpr int CBOX_BYTES = 16 * BN * 8;        // 8 KB: box of 16 rows x 64 cols
+constexpr int CBUF_BYTES = BM * BN * 8;        // 64 KB
+constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
+constexpr int BAR_BYTES = 256;
+constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
+constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
 
 struct Item {
   int64_t cTile, aTile0, bTile0;
   int64_t aStride, bStride;  // tile-index stride per k tile
   int nkt;                   // number of k tiles
   int mrow0, nrow0;          // row offsets inside the A / B tiles (= C block offsets)
-  int lower;                 // diagonal block of a diagonal tile: lower triangle only
+  int lower;                 // block straddles the diagonal of a diagonal tile
   bool valid;
 };
 
 __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
-  const int nbt = p.b / BM;
+  const int nblk = (p.b / BM) * (p.b / BN);
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
       const int64_t k = p.T - p.J - 1;
-      return k * (k + 1) / 2 * nbt * nbt;
+      return k * (k + 1) / 2 * nblk;
     }
     case GEMM_RECT_TRAIL:
-      return (int64_t)p.Tm * (p.T - p.J - 1) * nbt * nbt;
+      return (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
     case GEMM_SYRK_RECT:
-      return (int64_t)p.Tm * (p.Tm + 1) / 2 * nbt * nbt;
+      return (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
     default:
-      return p.count * nbt * nbt;
+      return p.count * nblk;
   }
 }
 
+// diagonal-tile block (bi, bj): skip blocks strictly above the diagonal,
+// mask the ones that straddle it
+__device__ __forceinline__ void diag_block(Item& it, int bi, int bj) {
+  if (bi * BM + BM - 1 < bj * BN) it.valid = false;
+  it.lower = (bi * BM < bj * BN + BN - 1);
+}
+
 __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) {
-  const int nbt = p.b / BM;
-  const int nb2 = nbt * nbt;
-  const int64_t t = item / nb2;
-  const int blk = (int)(item % nb2);
-  const int bi = blk / nbt, bj = blk % nbt;
+  const int nbn = p.b / BN;
+  const int nblk = (p.b / BM) * nbn;
+  const int64_t t = item / nblk;
+  const int blk = (int)(item % nblk);
+  const int bi = blk / nbn, bj = blk % nbn;
   Item it;
   it.mrow0 = bi * BM;
   it.nrow0 = bj * BN;
@@ -82,10 +107,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
       it.cTile = tri_index(R, C, p.T);
       it.aTile0 = tri_index(R, p.J, p.T);
       it.bTile0 = tri_index(C, p.J, p.T);
-      if (R == C) {
-        if (bi < bj) it.valid = false;
-        it.lower = (bi == bj);
-      }
+      if (R == C) diag_block(it, bi, bj);
       break;
     }
     case GEMM_RECT_TRAIL: {
@@ -104,10 +126,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
       it.bTile0 = cc;
       it.aStride = it.bStride = p.Tm;
       it.nkt = p.Tn;
-      if (rr == cc) {
-        if (bi < bj) it.valid = false;
-        it.lower = (bi == bj);
-      }
+      if (rr == cc) diag_block(it, bi, bj);
       break;
     }
     default: {  // GEMM_LIST: (C, A, B, lower) tile-index quadruples
@@ -115,195 +134,231 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
       it.cTile = q[0];
       it.aTile0 = q[1];
       it.bTile0 = q[2];
-      if (q[3]) {
-        if (bi < bj) it.valid = false;
-        it.lower = (bi == bj);
-      }
+      if (q[3]) diag_block(it, bi, bj);
       break;
     }
   }
   return it;
 }
 
-// byte offset of element (mn, k) inside one operand stage (8 boxes of 16x8)
-__device__ __forceinline__ uint32_t op_off(int mn, int k) {
-  return (uint32_t)((mn >> 4) * 1024 + k * 128 + ((((mn & 15) >> 1) ^ k) << 4) + ((mn & 1) << 3));
+// Per-lane byte offset of MMA fragment element (row p*8 + q of a 16-row TMA
+// box, k = 2*s4 + t) inside a 128B-swizzled box whose 128-byte lines are k
+// (operands) or n (C buffer): line*128 + (((p<<2) ^ ((q>>1) ^ k)) << 4) + (q&1)*8.
+__device__ __forceinline__ uint32_t lane_off(int p, int t, int q, int s4) {
+  const int k = 2 * s4 + t;
+  return (uint32_t)(k * 128 + ((((p << 2) ^ ((q >> 1) ^ k)) & 7) << 4) + ((q & 1) << 3));
 }
-// byte offset of element (m, n) inside the C buffer (8 boxes of 16x128)
-__device__ __forceinline__ uint32_t c_off(int m, int n) {
-  return (uint32_t)((m >> 4) * 16384 + n * 128 + ((((m & 15) >> 1) ^ (n & 7)) << 4) + ((m & 1) << 3));
+
+struct GroupSmem {
+  uint8_t* stages;
+  uint8_t* cbuf;
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* c_full;
+  uint64_t* c_empty;
+};
+
+__device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
+  GroupSmem gs;
+  gs.stages = smem + g * GROUP_BYTES;
+  gs.cbuf = gs.stages + STAGES * STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES + 2);
+  gs.full = bars;
+  gs.empty = bars + STAGES;
+  gs.c_full = bars + 2 * STAGES;
+  gs.c_empty = gs.c_full + 1;
+  return gs;
+}
+
+__device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const CUtensorMap* tmA,
+                                              const CUtensorMap* tmB, const CUtensorMap* tmC,
+                                              const GemmProblem& p, int64_t nitems, bool load_c) {
+  prefetch_tmap(tmA);
+  prefetch_tmap(tmB);
+  prefetch_tmap(tmC);
+  const uint64_t pol_keep = l2_policy_evict_last();
+  const uint64_t pol_stream = l2_policy_evict_first();
+  const int kc_per_tile = p.b / BK;
+  int stage = 0;
+  uint32_t phase = 0, cphase = 0;
+  for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
+       item += (int64_t)GROUPS * gridDim.x) {
+    const Item it = gemm_decode(p, item);
+    if (!it.valid) continue;
+    const int nk = it.nkt * kc_per_tile;
+    for (int kc = 0; kc < nk; ++kc) {
+      mbar_wait(&gs.empty[stage], phase ^ 1);
+      mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
+      const int kt = kc / kc_per_tile;
+      const int kin = (kc % kc_per_tile) * BK;
+      const int at = (int)(it.aTile0 + kt * it.aStride);
+      const int bt = (int)(it.bTile0 + kt * it.bStride);
+      uint8_t* sa = gs.stages + stage * STAGE_BYTES;
+      uint8_t* sb = sa + STAGE_A_BYTES;
+#pragma unroll
+      for (int i = 0; i < BM / 16; ++i)
+        tma_load_3d(sa + i * 1024, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
+#pragma unroll
+      for (int i = 0; i < BN / 16; ++i)
+        tma_load_3d(sb + i * 1024, tmB, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (load_c && kc == (nk > 1 ? 1 : 0)) {
+        // C block for the epilogue, once the previous store has drained it
+        mbar_wait(gs.c_empty, cphase ^ 1);
+        mbar_arrive_expect_tx(gs.c_full, CBUF_BYTES);
+#pragma unroll
+        for (int i = 0; i < BM / 16; ++i)
+          tma_load_3d(gs.cbuf + i * CBOX_BYTES, tmC, gs.c_full, it.mrow0 + i * 16, it.nrow0, (int)it.cTile,
+                      pol_stream);
+        cphase ^= 1;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
+                                              const CUtensorMap* tmC, const GemmProblem& p, int64_t nitems,
+                                              bool load_c) {
+  const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
+  const int q = lane >> 2, s4 = lane & 3;
+  const bool leader = (gwarp == 0 && lane == 0);
+  const int bar_id = 1 + g;
+  const int kc_per_tile = p.b / BK;
+  uint32_t offA[2][2], offB[2][2];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      offA[pp][t] = (uint32_t)(wm * (WM / 16) * 1024) + lane_off(pp, t, q, s4);
+      offB[pp][t] = (uint32_t)(STAGE_A_BYTES + wn * (WN / 16) * 1024) + lane_off(pp, t, q, s4);
+    }
+  int stage = 0;
+  uint32_t phase = 0, cphase = 0;
+  bool store_pending = false;
+  const uint64_t pol_stream = l2_policy_evict_first();
+
+  for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
+       item += (int64_t)GROUPS * gridDim.x) {
+    const Item it = gemm_decode(p, item);
+    if (!it.valid) continue;
+    const int nk = it.nkt * kc_per_tile;
+    double acc[MI][NJ][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kc = 0; kc < nk; ++kc) {
+      mbar_wait(&gs.full[stage], phase);
+      const uint8_t* st = gs.stages + stage * STAGE_BYTES;
+      double af[2][MI], bf[2][NJ];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+          af[t][i] = *reinterpret_cast<const double*>(st + offA[i & 1][t] + (i >> 1) * 1024);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          bf[t][j] = *reinterpret_cast<const double*>(st + offB[j & 1][t] + (j >> 1) * 1024);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gs.empty[stage]);  // fragments are in registers
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[t][i], bf[t][j]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (kc == 0 && store_pending && leader) {
+        // previous block's TMA store has to finish reading the C buffer
+        // before the producer may overwrite it
+        tma_store_wait_read0();
+        mbar_arrive(gs.c_empty);
+      }
+    }
+
+    // ------------------------------- epilogue -------------------------------
+    if (load_c) {
+      mbar_wait(gs.c_full, cphase);
+    } else {
+      if (store_pending && leader) tma_store_wait_read0();
+      named_bar_sync(bar_id, GROUP_WARPS * 32);
+    }
+    cphase ^= 1;
+    uint8_t* cw = gs.cbuf + wm * (WM / 16) * CBOX_BYTES + wn * WN * 128;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int m = it.mrow0 + wm * WM + i * 8 + q;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
+          double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * CBOX_BYTES +
+                                                  j * 8 * 128);
+          const double cv = load_c ? *ptr : 0.0;
+          double d;
+          if (it.lower && m < n) d = cv;  // keep the strict upper triangle
+          else d = load_c ? fma(p.alpha, acc[i][j][e], p.beta * cv) : p.alpha * acc[i][j][e];
+          *ptr = d;
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(bar_id, GROUP_WARPS * 32);
+    if (leader) {
+#pragma unroll
+      for (int i = 0; i < BM / 16; ++i)
+        tma_store_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile, pol_stream);
+      tma_store_commit();
+    }
+    store_pending = true;
+  }
+  if (leader && store_pending) tma_store_wait_all0();
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmProblem p,
                      const unsigned long long* __restrict__ info) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* stages = smem;
-  uint8_t* cbuf = smem + STAGES * STAGE_BYTES;
-  uint64_t* bars = (uint64_t*)(cbuf + CBUF_BYTES);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* c_full = bars + 2 * STAGES;
-  uint64_t* c_empty = c_full + 1;
-
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
   if (info && *(volatile const unsigned long long*)info != 0ull) return;  // factorization failed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wg = warp >> 2;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MMA_WARPS);
+    for (int g = 0; g < GROUPS; ++g) {
+      GroupSmem gs = group_smem(smem, g);
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&gs.full[s], 1);
+        mbar_init(&gs.empty[s], GROUP_WARPS);
+      }
+      mbar_init(gs.c_full, 1);
+      mbar_init(gs.c_empty, 1);
     }
-    mbar_init(c_full, 1);
-    mbar_init(c_empty, 1);
     fence_barrier_init();
   }
   __syncthreads();
 
   const int64_t nitems = gemm_num_items(p);
-  const int kc_per_tile = p.b / BK;
   const bool load_c = (p.beta != 0.0);
-
-  if (warp == MMA_WARPS) {
-    // ------------------------------ producer ------------------------------
-    if (lane == 0) {
-      prefetch_tmap(&tmA);
-      prefetch_tmap(&tmB);
-      prefetch_tmap(&tmC);
-      const uint64_t pol_keep = l2_policy_evict_last();
-      const uint64_t pol_stream = l2_policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0, cphase = 0;
-      for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-        const Item it = gemm_decode(p, item);
-        if (!it.valid) continue;
-        const int nk = it.nkt * kc_per_tile;
-        for (int kc = 0; kc < nk; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          const int kt = kc / kc_per_tile;
-          const int kin = (kc % kc_per_tile) * BK;
-          const int at = (int)(it.aTile0 + kt * it.aStride);
-          const int bt = (int)(it.bTile0 + kt * it.bStride);
-          uint8_t* sa = stages + stage * STAGE_BYTES;
-          uint8_t* sb = sa + STAGE_A_BYTES;
-#pragma unroll
-          for (int i = 0; i < BM / 16; ++i)
-            tma_load_3d(sa + i * 1024, &tmA, &full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
-#pragma unroll
-          for (int i = 0; i < BN / 16; ++i)
-            tma_load_3d(sb + i * 1024, &tmB, &full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (load_c && kc == (nk > 1 ? 1 : 0)) {
-            mbar_wait(c_empty, cphase ^ 1);
-            mbar_arrive_expect_tx(c_full, CBUF_BYTES);
-#pragma unroll
-            for (int i = 0; i < BM / 16; ++i)
-              tma_load_3d(cbuf + i * 16384, &tmC, c_full, it.mrow0 + i * 16, it.nrow0, (int)it.cTile,
-                          pol_stream);
-            cphase ^= 1;
-          }
-        }
-      }
-    }
-    return;
+  if (wg == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+    if (warp < GROUPS && lane == 0)
+      producer_loop(group_smem(smem, warp), warp, &tmA, &tmB, &tmC, p, nitems, load_c);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+    const int g = wg - 1;
+    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, load_c);
   }
-
-  // -------------------------------- MMA warps --------------------------------
-  const int wm = warp / (BN / WN), wn = warp % (BN / WN);
-  const int q = lane >> 2, s4 = lane & 3;
-  int stage = 0;
-  uint32_t phase = 0, cphase = 0;
-  bool store_pending = false;
-  const uint32_t stages_u32 = smem_u32(stages);
-  const uint32_t cbuf_u32 = smem_u32(cbuf);
-  const uint64_t pol_stream = l2_policy_evict_first();
-
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const Item it = gemm_decode(p, item);
-    if (!it.valid) continue;
-    const int nk = it.nkt * kc_per_tile;
-    double acc[WM / 8][WN / 8][2];
-#pragma unroll
-    for (int i = 0; i < WM / 8; ++i)
-#pragma unroll
-      for (int j = 0; j < WN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    for (int kc = 0; kc < nk; ++kc) {
-      mbar_wait(&full[stage], phase);
-      const uint32_t sa = stages_u32 + stage * STAGE_BYTES;
-      const uint32_t sb = sa + STAGE_A_BYTES;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int k = 2 * s4 + t;
-        double af[WM / 8], bf[WN / 8];
-#pragma unroll
-        for (int i = 0; i < WM / 8; ++i)
-          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(af[i]) : "r"(sa + op_off(wm * WM + i * 8 + q, k)));
-#pragma unroll
-        for (int j = 0; j < WN / 8; ++j)
-          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bf[j]) : "r"(sb + op_off(wn * WN + j * 8 + q, k)));
-#pragma unroll
-        for (int i = 0; i < WM / 8; ++i)
-#pragma unroll
-          for (int j = 0; j < WN / 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1;
-      }
-      if (kc == 0 && store_pending && threadIdx.x == 0) {
-        // previous block's TMA store has to finish reading the C buffer
-        // before the producer may overwrite it
-        tma_store_wait_read0();
-        mbar_arrive(c_empty);
-      }
-    }
-
-    // ------------------------------- epilogue -------------------------------
-    if (load_c) {
-      mbar_wait(c_full, cphase);
-    } else {
-      if (store_pending && threadIdx.x == 0) tma_store_wait_read0();
-      named_bar_sync(1, MMA_WARPS * 32);
-    }
-    cphase ^= 1;
-#pragma unroll
-    for (int i = 0; i < WM / 8; ++i) {
-#pragma unroll
-      for (int j = 0; j < WN / 8; ++j) {
-        const int m = wm * WM + i * 8 + q;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = wn * WN + j * 8 + 2 * s4 + e;
-          const uint32_t addr = cbuf_u32 + c_off(m, n);
-          double cv = 0.0;
-          if (load_c) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cv) : "r"(addr));
-          double d;
-          if (it.lower && m < n) d = load_c ? cv : 0.0;  // keep the strict upper triangle
-          else d = load_c ? fma(p.alpha, acc[i][j][e], p.beta * cv) : p.alpha * acc[i][j][e];
-          asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(d) : "memory");
-        }
-      }
-    }
-    fence_proxy_async_smem();
-    named_bar_sync(1, MMA_WARPS * 32);
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int i = 0; i < BM / 16; ++i)
-        tma_store_3d(&tmC, cbuf + i * 16384, it.mrow0 + i * 16, it.nrow0, (int)it.cTile, pol_stream);
-      tma_store_commit();
-    }
-    store_pending = true;
-  }
-  if (threadIdx.x == 0 && store_pending) tma_store_wait_all0();
 }
 
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
@@ -311,21 +366,21 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
   if (p.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
   int64_t items;
   {
-    const int nbt = p.b / BM;
+    const int64_t nblk = (int64_t)(p.b / BM) * (p.b / BN);
     switch (p.mode) {
       case GEMM_CHOL_TRAIL: {
         const int64_t k = p.T - p.J - 1;
-        items = k * (k + 1) / 2 * nbt * nbt;
+        items = k * (k + 1) / 2 * nblk;
         break;
       }
       case GEMM_RECT_TRAIL:
-        items = (int64_t)p.Tm * (p.T - p.J - 1) * nbt * nbt;
+        items = (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
         break;
       case GEMM_SYRK_RECT:
-        items = (int64_t)p.Tm * (p.Tm + 1) / 2 * nbt * nbt;
+        items = (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
         break;
       default:
-        items = p.count * nbt * nbt;
+        items = p.count * nblk;
     }
   }
   if (items <= 0) return BGP_OK;
@@ -334,12 +389,15 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
   if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, BN, true)) != BGP_OK) return rc;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static int occupancy = -1;
+  if (occupancy < 0) {
     cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr_done = true;
+    cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, gemm_dmma_kernel, THREADS, SMEM_BYTES);
+    if (occupancy < 1) fprintf(stderr, "libbgp: gemm_dmma_kernel cannot be resident\n");
   }
-  const int64_t grid = items < ctx->num_sms ? items : ctx->num_sms;
+  const int64_t slots = ctx->num_sms;
+  const int64_t grid = items < slots ? items : slots;
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mC, p, ctx->d_info);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");
