@@ -168,6 +168,27 @@ int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out,
  *   lower != 0 updates only the lower triangle (diagonal SYRK). */
 int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0,
                    int64_t* info, void* stream);
+/* A rank's share of construct: lower tiles (I, J) listed in tile_ij (device,
+ * 2 int32 per tile) written to consecutive b x b tiles of out
+ * (bg/distla/kernels.py:45-75 over this rank's owned blocks). */
+int bgp_construct_tiles(bgp_ctx_t ctx, const bgp_generator* gen, const double* X,
+                        int64_t n, int dim, int tile, const int32_t* tile_ij,
+                        int64_t count, double* out, void* stream);
+/* Diagonal-tile solve of a distributed TRSV step: x (b doubles) <- L_jj^{-1} x
+ * or L_jj^{-T} x; row0 = global row of the tile (kernels.py:244-249). */
+int bgp_tile_trsv(bgp_ctx_t ctx, const double* Ljj, int tile, int64_t row0,
+                  int64_t n, double* x, int trans, int64_t* info, void* stream);
+/* acc[target*b ...] += L_tile x_J (trans 0) or L_tile^T x_J (trans 1) for
+ * (tile index, target block) pairs (device, distinct targets): the partial
+ * products of solve_vector (kernels.py:219-235). */
+int bgp_tile_gemv(bgp_ctx_t ctx, const double* base, const int32_t* items,
+                  int64_t count, int tile, const double* xJ, double* acc,
+                  int trans, void* stream);
+/* Per-rank log-det partial over listed diagonal tiles (tile index, J)
+ * (kernels.py:493-509). */
+int bgp_tile_logdet(bgp_ctx_t ctx, const double* base, const int32_t* diag,
+                    int64_t count, int tile, int64_t n, double* out,
+                    int64_t* info, void* stream);
 int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count,
                    int tile, void* stream);
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,

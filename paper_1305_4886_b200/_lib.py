@@ -63,6 +63,13 @@ SIGNATURES = {
     "bgp_tile_potrf": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, ctypes.POINTER(_i64), _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
+    "bgp_construct_tiles": (_int, [ctypes.c_void_p, ctypes.POINTER(Generator), _c_dp, _i64, _int, _int,
+                                   _c_dp, _i64, _c_dp, _c_dp]),
+    "bgp_tile_trsv": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, _i64, _c_dp, _int,
+                             ctypes.POINTER(_i64), _c_dp]),
+    "bgp_tile_gemv": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp, _c_dp, _int, _c_dp]),
+    "bgp_tile_logdet": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _i64,
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), _c_dp]),
     "bgp_set_profiling": (_int, [ctypes.c_void_p, _int]),
     "bgp_profile_read": (_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
 }

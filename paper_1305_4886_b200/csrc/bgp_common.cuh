@@ -18,12 +18,13 @@ __host__ __device__ __forceinline__ int64_t tri_index(int64_t I, int64_t J, int6
 __host__ __device__ __forceinline__ int64_t tri_count(int64_t T) { return T * (T + 1) / 2; }
 
 // flat index t over the lower triangle of a k x k tile grid, column-major
-// -> (r, c) with r >= c
+// -> (r, c) with r >= c.  FP32 estimate + integer correction, so no FP64
+// instruction competes with the DMMA pipe.
 __device__ __forceinline__ void tri_decode(int64_t t, int64_t k, int& r, int& c) {
   // column c holds k - c entries; start(c) = c*k - c*(c-1)/2
-  double kk = (double)k + 0.5;
-  double disc = kk * kk - 2.0 * (double)t;
-  int cc = (int)(kk - sqrt(disc > 0 ? disc : 0.0));
+  const float kk = (float)k + 0.5f;
+  const float disc = kk * kk - 2.0f * (float)t;
+  int cc = (int)(kk - sqrtf(disc > 0.f ? disc : 0.f));
   if (cc < 0) cc = 0;
   if (cc > k - 1) cc = (int)k - 1;
   while (cc > 0 && (int64_t)cc * k - (int64_t)cc * (cc - 1) / 2 > t) --cc;

@@ -55,6 +55,15 @@ int make_tile_map(Ctx* ctx, CUtensorMap* map, const double* base, int b, int64_t
 int construct(Ctx* ctx, int kind, const GenDev& g, const double* X, int64_t nx, const double* Y,
               int64_t ny, int b, double* out, cudaStream_t s);
 
+int construct_tiles(Ctx* ctx, const GenDev& g, const double* X, int64_t n, int b, const int32_t* tile_ij,
+                    int64_t count, double* out, cudaStream_t s);
+int launch_tile_trsv(Ctx* ctx, const double* Ljj, int b, int64_t row0, int64_t n, double* x, int trans,
+                     cudaStream_t s);
+int launch_tile_gemv(Ctx* ctx, const double* base, const int32_t* items, int64_t count, int b, const double* xJ,
+                     double* partial, int trans, cudaStream_t s);
+int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_t count, int b, int64_t n,
+                       cudaStream_t s);
+
 // tile kernels
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);

@@ -382,6 +382,47 @@ int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out, int64_
   return launch_sub(ctx, a, b, out, count, (cudaStream_t)stream);
 }
 
+int bgp_construct_tiles(bgp_ctx_t ctx, const bgp_generator* gen, const double* X, int64_t n, int dim, int tile,
+                        const int32_t* tile_ij, int64_t count, double* out, void* stream) {
+  if (!valid_tile(tile) || n < 1 || count < 0) return BGP_E_ARG;
+  GenDev g;
+  int rc = to_gendev(ctx, gen, dim, &g);
+  if (rc) return rc;
+  return construct_tiles(ctx, g, X, n, tile, tile_ij, count, out, (cudaStream_t)stream);
+}
+
+int bgp_tile_trsv(bgp_ctx_t ctx, const double* Ljj, int tile, int64_t row0, int64_t n, double* x, int trans,
+                  int64_t* info, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  if ((rc = launch_tile_trsv(ctx, Ljj, tile, row0, n, x, trans, s))) return rc;
+  return read_info(ctx, s, info);
+}
+
+int bgp_tile_gemv(bgp_ctx_t ctx, const double* base, const int32_t* items, int64_t count, int tile,
+                  const double* xJ, double* acc, int trans, void* stream) {
+  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
+  return launch_tile_gemv(ctx, base, items, count, tile, xJ, acc, trans, (cudaStream_t)stream);
+}
+
+int bgp_tile_logdet(bgp_ctx_t ctx, const double* base, const int32_t* diag, int64_t count, int tile, int64_t n,
+                    double* out, int64_t* info, void* stream) {
+  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  if (count == 0) {
+    *out = 0.0;
+    return read_info(ctx, s, info);
+  }
+  if ((rc = launch_tile_logdet(ctx, base, diag, count, tile, n, s))) return rc;
+  cudaError_t e = cudaMemcpyAsync(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return set_err(ctx, "tile_logdet copy", e);
+  return read_info(ctx, s, info);
+}
+
 int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0, int64_t* info, void* stream) {
   if (!valid_tile(tile)) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

@@ -77,14 +77,21 @@ __device__ __forceinline__ double gen_eval(const GenDev& g, const double* xi, co
 
 constexpr int kCovThreads = 256;
 
-// triangular: one CTA per lower tile (flat packed index)
+// triangular: one CTA per lower tile (flat packed index, or an explicit
+// (I, J) list for a rank's share of a 2-D block-cyclic distribution)
 template <bool kPts>
 __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const double* __restrict__ X,
                                                               int64_t n, int T, int b,
-                                                              double* __restrict__ out) {
+                                                              double* __restrict__ out,
+                                                              const int32_t* __restrict__ tile_ij) {
   extern __shared__ double colpts[];  // b * dim
   int I, J;
-  tri_decode(blockIdx.x, T, I, J);
+  if (tile_ij) {
+    I = tile_ij[2 * blockIdx.x];
+    J = tile_ij[2 * blockIdx.x + 1];
+  } else {
+    tri_decode(blockIdx.x, T, I, J);
+  }
   const int dim = g.dim;
   const int64_t j0 = (int64_t)J * b, i0 = (int64_t)I * b;
   for (int t = threadIdx.x; t < b * dim; t += blockDim.x) {
@@ -164,9 +171,9 @@ int construct(Ctx* ctx, int kind, const GenDev& g, const double* X, int64_t nx, 
   if (kind == BGP_TRI) {
     int T = (int)((nx + b - 1) / b);
     if (X)
-      cov_tri_kernel<true><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out);
+      cov_tri_kernel<true><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out, nullptr);
     else
-      cov_tri_kernel<false><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out);
+      cov_tri_kernel<false><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out, nullptr);
   } else if (kind == BGP_RECT) {
     int Tn = (int)((nx + b - 1) / b), Tm = (int)((ny + b - 1) / b);
     const unsigned grid = (unsigned)((int64_t)Tn * Tm);
@@ -180,6 +187,19 @@ int construct(Ctx* ctx, int kind, const GenDev& g, const double* X, int64_t nx, 
   }
   ctx->launches++;
   return check_launch(ctx, "construct");
+}
+
+int construct_tiles(Ctx* ctx, const GenDev& g, const double* X, int64_t n, int b, const int32_t* tile_ij,
+                    int64_t count, double* out, cudaStream_t s) {
+  if (count <= 0) return BGP_OK;
+  const size_t smem = (size_t)b * (g.dim > 0 ? g.dim : 1) * sizeof(double);
+  const int T = (int)((n + b - 1) / b);
+  if (X)
+    cov_tri_kernel<true><<<(unsigned)count, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij);
+  else
+    cov_tri_kernel<false><<<(unsigned)count, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij);
+  ctx->launches++;
+  return check_launch(ctx, "construct_tiles");
 }
 
 }  // namespace bgp

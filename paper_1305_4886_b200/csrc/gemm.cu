@@ -303,11 +303,10 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
           const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
           double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * CBOX_BYTES +
                                                   j * 8 * 128);
+          // alpha/beta are (-1, 1) (updates) or (1, 0) (V^T V): C - acc or acc
           const double cv = load_c ? *ptr : 0.0;
-          double d;
-          if (it.lower && m < n) d = cv;  // keep the strict upper triangle
-          else d = load_c ? fma(p.alpha, acc[i][j][e], p.beta * cv) : p.alpha * acc[i][j][e];
-          *ptr = d;
+          const bool keep = it.lower && m < n;  // strict upper triangle stays
+          *ptr = keep ? cv : (load_c ? cv - acc[i][j][e] : acc[i][j][e]);
         }
       }
     }

@@ -17,14 +17,12 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
 // forward: solve L_JJ x_J = r_J in place (one CTA), zero diagonal -> info
-__global__ void __launch_bounds__(256) trsv_diag_fwd_kernel(const double* __restrict__ L, int T, int b,
-                                                            int64_t n, int J, double* __restrict__ x,
+__global__ void __launch_bounds__(256) trsv_diag_fwd_kernel(const double* __restrict__ tile, int b,
+                                                            int64_t n, int64_t row0, double* __restrict__ xj,
                                                             unsigned long long* __restrict__ info) {
   __shared__ double xs[512];
   __shared__ int s_fail;
   if (*(volatile unsigned long long*)info != 0ull) return;
-  const double* tile = L + tri_index(J, J, T) * (int64_t)b * b;
-  double* xj = x + (int64_t)J * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_fail = 0;
   for (int i = tid; i < b; i += blockDim.x) xs[i] = xj[i];
@@ -34,10 +32,10 @@ __global__ void __launch_bounds__(256) trsv_diag_fwd_kernel(const double* __rest
       // lane = row c0+lane; sequential over the 32 columns
       double r = xs[c0 + lane];
       const double dii = tile[(int64_t)(c0 + lane) * b + c0 + lane];
-      const unsigned z = __ballot_sync(FULLM, dii == 0.0 && ((int64_t)J * b + c0 + lane) < n);
+      const unsigned z = __ballot_sync(FULLM, dii == 0.0 && (row0 + c0 + lane) < n);
       if (z) {
         if (lane == 0) {
-          set_info(info, (int64_t)J * b + c0 + __ffs(z));
+          set_info(info, row0 + c0 + __ffs(z));
           s_fail = 1;
         }
       } else {
@@ -87,14 +85,12 @@ __global__ void __launch_bounds__(256) trsv_update_fwd_kernel(const double* __re
 }
 
 // back: solve L_JJ^T x_J = r_J in place (one CTA)
-__global__ void __launch_bounds__(256) trsv_diag_back_kernel(const double* __restrict__ L, int T, int b,
-                                                             int64_t n, int J, double* __restrict__ x,
+__global__ void __launch_bounds__(256) trsv_diag_back_kernel(const double* __restrict__ tile, int b,
+                                                             int64_t n, int64_t row0, double* __restrict__ xj,
                                                              unsigned long long* __restrict__ info) {
   __shared__ double xs[512];
   __shared__ int s_fail;
   if (*(volatile unsigned long long*)info != 0ull) return;
-  const double* tile = L + tri_index(J, J, T) * (int64_t)b * b;
-  double* xj = x + (int64_t)J * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_fail = 0;
   for (int i = tid; i < b; i += blockDim.x) xs[i] = xj[i];
@@ -103,10 +99,10 @@ __global__ void __launch_bounds__(256) trsv_diag_back_kernel(const double* __res
     if (warp == 0) {
       double r = xs[c0 + lane];
       const double dii = tile[(int64_t)(c0 + lane) * b + c0 + lane];
-      const unsigned z = __ballot_sync(FULLM, dii == 0.0 && ((int64_t)J * b + c0 + lane) < n);
+      const unsigned z = __ballot_sync(FULLM, dii == 0.0 && (row0 + c0 + lane) < n);
       if (z) {
         if (lane == 0) {
-          set_info(info, (int64_t)J * b + c0 + 32 - __clz(z));
+          set_info(info, row0 + c0 + 32 - __clz(z));
           s_fail = 1;
         }
       } else {
@@ -158,7 +154,8 @@ int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int tran
   const int T = (int)((n + b - 1) / b);
   if (!trans) {
     for (int J = 0; J < T; ++J) {
-      trsv_diag_fwd_kernel<<<1, 256, 0, s>>>(L, T, b, n, J, x, ctx->d_info);
+      trsv_diag_fwd_kernel<<<1, 256, 0, s>>>(L + tri_index(J, J, T) * (int64_t)b * b, b, n, (int64_t)J * b,
+                                             x + (int64_t)J * b, ctx->d_info);
       ctx->launches++;
       if (J + 1 < T) {
         trsv_update_fwd_kernel<<<T - J - 1, 256, 0, s>>>(L, T, b, J, x, ctx->d_info);
@@ -167,7 +164,8 @@ int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int tran
     }
   } else {
     for (int J = T - 1; J >= 0; --J) {
-      trsv_diag_back_kernel<<<1, 256, 0, s>>>(L, T, b, n, J, x, ctx->d_info);
+      trsv_diag_back_kernel<<<1, 256, 0, s>>>(L + tri_index(J, J, T) * (int64_t)b * b, b, n, (int64_t)J * b,
+                                              x + (int64_t)J * b, ctx->d_info);
       ctx->launches++;
       if (J > 0) {
         trsv_update_back_kernel<<<J, 256, 0, s>>>(L, T, b, J, x, ctx->d_info);
@@ -231,6 +229,86 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLM, v, o);
   }
   return v;
+}
+
+// tile-list forms for the multi-GPU driver ------------------------------------
+int launch_tile_trsv(Ctx* ctx, const double* Ljj, int b, int64_t row0, int64_t n, double* x, int trans,
+                     cudaStream_t s) {
+  if (!trans) trsv_diag_fwd_kernel<<<1, 256, 0, s>>>(Ljj, b, n, row0, x, ctx->d_info);
+  else trsv_diag_back_kernel<<<1, 256, 0, s>>>(Ljj, b, n, row0, x, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "tile_trsv");
+}
+
+// acc[target] += L_tile x (trans 0) or L_tile^T x (trans 1); items = (tile
+// index, target block) pairs with distinct targets
+__global__ void __launch_bounds__(256) tile_gemv_kernel(const double* __restrict__ base,
+                                                        const int32_t* __restrict__ items, int b,
+                                                        const double* __restrict__ xJ,
+                                                        double* __restrict__ acc, int trans) {
+  __shared__ double xs[512];
+  const double* tile = base + (int64_t)items[2 * blockIdx.x] * b * b;
+  double* out = acc + (int64_t)items[2 * blockIdx.x + 1] * b;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) xs[i] = xJ[i];
+  __syncthreads();
+  if (!trans) {
+    for (int i = threadIdx.x; i < b; i += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int k = 0; k < b; k += 2) {
+        a0 = fma(tile[(int64_t)k * b + i], xs[k], a0);
+        a1 = fma(tile[(int64_t)(k + 1) * b + i], xs[k + 1], a1);
+      }
+      out[i] += a0 + a1;
+    }
+  } else {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = warp; k < b; k += nw) {
+      double a = 0.0;
+      for (int i = lane; i < b; i += 32) a = fma(tile[(int64_t)k * b + i], xs[i], a);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULLM, a, o);
+      if (lane == 0) out[k] += a;
+    }
+  }
+}
+
+int launch_tile_gemv(Ctx* ctx, const double* base, const int32_t* items, int64_t count, int b, const double* xJ,
+                     double* partial, int trans, cudaStream_t s) {
+  if (count <= 0) return BGP_OK;
+  tile_gemv_kernel<<<(unsigned)count, 256, 0, s>>>(base, items, b, xJ, partial, trans);
+  ctx->launches++;
+  return check_launch(ctx, "tile_gemv");
+}
+
+// 2 sum log L_ii over the live rows of listed diagonal tiles (tile index, J)
+__global__ void __launch_bounds__(1024) tile_logdet_kernel(const double* __restrict__ base,
+                                                           const int32_t* __restrict__ diag, int64_t count, int b,
+                                                           int64_t n, double* __restrict__ out,
+                                                           unsigned long long* __restrict__ info) {
+  __shared__ double sh[32];
+  double s = 0.0, c = 0.0;
+  const int64_t total = count * b;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t k = e / b;
+    const int r = (int)(e % b);
+    const int64_t row = (int64_t)diag[2 * k + 1] * b + r;
+    if (row >= n) continue;
+    const double d = base[(int64_t)diag[2 * k] * b * b + (int64_t)r * b + r];
+    if (!(d > 0.0)) set_info(info, row + 1);
+    const double y = log(d) - c;
+    const double t = s + y;
+    c = (t - s) - y;
+    s = t;
+  }
+  const double tot = block_sum<1024>(s, sh);
+  if (threadIdx.x == 0) out[0] = 2.0 * tot;
+}
+
+int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_t count, int b, int64_t n,
+                       cudaStream_t s) {
+  tile_logdet_kernel<<<1, 1024, 0, s>>>(base, diag, count, b, n, ctx->d_red, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "tile_logdet");
 }
 
 // 2 * sum_{i<n} log L_ii; Kahan per thread, fixed-shape tree across threads

@@ -49,6 +49,7 @@ class DevObj:
     col_layout: Optional[BlockLayout]
     tile: int
     data: Any
+    dist: Any = None   # parallel.TileDist when the tiles are spread over G > 1 GPUs
 
     @property
     def n(self):

@@ -39,11 +39,38 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _need(ctx, name, kind):
+def _need(ctx, name, kind, full=True):
     obj = ctx.fetch(name)
     if not isinstance(obj, DevObj) or obj.kind != kind:
         raise DimensionMismatch(f"object {name!r} is not a device {kind} object")
-    return obj
+    return _full(ctx, obj) if full else obj
+
+
+def _packed_index(dist):
+    import torch
+    I = dist.tiles[:, 0].astype(np.int64)
+    J = dist.tiles[:, 1].astype(np.int64)
+    T = dist.T
+    return torch.from_numpy(J * T - J * (J - 1) // 2 + (I - J))
+
+
+def _full(ctx, obj):
+    """Replicated packed copy of a distributed triangular object (for the
+    operations that run on one GPU's full copy: collect, kriging solves,
+    crossproducts, elementwise helpers)."""
+    if obj.dist is None:
+        return obj
+    d = obj.dist
+    full = ctx.zeros((d.T * (d.T + 1) // 2, obj.tile, obj.tile))
+    if d.count:
+        full.index_copy_(0, _packed_index(d).to(full.device), obj.data[:d.count])
+    ctx.comm.all_reduce_sum(full)
+    return DevObj(obj.kind, obj.row_layout, obj.col_layout, obj.tile, full)
+
+
+def _tile_ops(ctx, n):
+    from ..parallel import LibTileOps
+    return LibTileOps(ctx, n)
 
 
 # ---------------------------------------------------------------------------
@@ -111,9 +138,19 @@ def construct(ctx, name, kind, generator, params, inputs_name, row_layout, col_l
             Y = ctx.device_input(inputs_name, "pred_coords")
             if Y.shape[1] != dim or Y.shape[0] < m:
                 raise GeneratorError(ctx.rank, IndexError("pred_coords do not conform"))
-    out = _alloc(ctx, kind, n, m)
     if name in ctx.store:
         del ctx.store[name]
+    if kind == "triangular" and ctx.G > 1:
+        from ..parallel import TileDist
+        td = TileDist(n, ctx.tile, ctx.grid, ctx.rank - 1)
+        out = ctx.empty((max(td.count, 1), ctx.tile, ctx.tile))
+        tij = ctx.upload_int32(td.tiles)
+        ctx.call("bgp_construct_tiles", ctypes.byref(desc), _ptr(X) if X is not None else None, n, dim,
+                 ctx.tile, _ptr(tij), td.count, _ptr(out), ctx.stream)
+        ctx.store[name] = DevObj(kind, row_layout, col_layout or row_layout, ctx.tile, out, td)
+        ctx.log_event("construct")
+        return
+    out = _alloc(ctx, kind, n, m)
     ctx.call("bgp_construct", _lib.KIND_CODE[kind], ctypes.byref(desc),
              _ptr(X) if X is not None else None, n,
              _ptr(Y) if Y is not None else None, m or 0, dim, ctx.tile, _ptr(out), ctx.stream)
@@ -145,7 +182,12 @@ def split(ctx, name, kind, array, row_layout, col_layout=None):
     ctx.call("bgp_pack", _lib.KIND_CODE[kind], _ptr(dense), n, m or 1, ld, ctx.tile,
              _ptr(out), ctx.stream)
     cl = (col_layout or row_layout) if kind != "vector" else None
-    ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out)
+    td = None
+    if kind == "triangular" and ctx.G > 1:
+        from ..parallel import TileDist
+        td = TileDist(n, ctx.tile, ctx.grid, ctx.rank - 1)
+        out = out.index_select(0, _packed_index(td).to(out.device)).contiguous()
+    ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out, td)
 
 
 # ---------------------------------------------------------------------------
@@ -153,13 +195,17 @@ def split(ctx, name, kind, array, row_layout, col_layout=None):
 
 @registry.register("distla.cholesky")
 def cholesky(ctx, name, out_name):
-    obj = _need(ctx, name, "triangular")
+    obj = _need(ctx, name, "triangular", full=False)
     if out_name != name:
         ctx.store[out_name] = obj
         del ctx.store[name]
     info = ctypes.c_int64(0)
     try:
-        ctx.call("bgp_potrf", _ptr(obj.data), obj.n, obj.tile, ctypes.byref(info), ctx.stream)
+        if obj.dist is not None:
+            from ..parallel import dist_cholesky
+            info.value = dist_cholesky(obj.dist, obj.data, _tile_ops(ctx, obj.n), ctx.comm)
+        else:
+            ctx.call("bgp_potrf", _ptr(obj.data), obj.n, obj.tile, ctypes.byref(info), ctx.stream)
     except BaseException:
         ctx.store.pop(out_name, None)  # no partial factor is retained
         raise
@@ -167,7 +213,7 @@ def cholesky(ctx, name, out_name):
         ctx.store.pop(out_name, None)
         raise NotPositiveDefinite((info.value - 1) // obj.row_layout.block_size + 1)
     ctx.log_event("factor")
-    nt = obj.data.shape[0]
+    nt = obj.dist.count if obj.dist is not None else obj.data.shape[0]
     return {"peak_blocks": nt, "owned_blocks": nt, "tile": obj.tile}
 
 
@@ -176,14 +222,18 @@ def cholesky(ctx, name, out_name):
 
 @registry.register("distla.solve_vector")
 def solve_vector(ctx, l_name, rhs_name, out_name, forward=True):
-    L = _need(ctx, l_name, "triangular")
+    L = _need(ctx, l_name, "triangular", full=False)
     rhs = _need(ctx, rhs_name, "vector")
-    if rhs.data.shape[0] != L.data.shape[1] * _ntiles(L.n, L.tile) or rhs.n != L.n:
+    if rhs.data.shape[0] != L.tile * _ntiles(L.n, L.tile) or rhs.n != L.n:
         raise DimensionMismatch("rhs does not conform to L")
-    x = rhs.data.clone()
     info = ctypes.c_int64(0)
-    ctx.call("bgp_trsv", _ptr(L.data), L.n, L.tile, _ptr(x), 0 if forward else 1,
-             ctypes.byref(info), ctx.stream)
+    if L.dist is not None:
+        from ..parallel import dist_trsv
+        x, info.value = dist_trsv(L.dist, L.data, rhs.data, _tile_ops(ctx, L.n), ctx.comm, forward)
+    else:
+        x = rhs.data.clone()
+        ctx.call("bgp_trsv", _ptr(L.data), L.n, L.tile, _ptr(x), 0 if forward else 1,
+                 ctypes.byref(info), ctx.stream)
     if info.value:
         raise SingularDiagonal(f"zero diagonal at row {info.value}")
     ctx.store[out_name] = DevObj("vector", rhs.row_layout, None, rhs.tile, x)
@@ -241,7 +291,13 @@ def xprod_self_diag(ctx, v_name, out_name):
 
 @registry.register("distla.logdet")
 def logdet(ctx, l_name):
-    L = _need(ctx, l_name, "triangular")
+    L = _need(ctx, l_name, "triangular", full=False)
+    if L.dist is not None:
+        from ..parallel import dist_logdet
+        value, info = dist_logdet(L.dist, L.data, _tile_ops(ctx, L.n), ctx.comm)
+        if info:
+            raise SingularDiagonal(f"non-positive diagonal at row {info}")
+        return value
     out = ctypes.c_double(0.0)
     info = ctypes.c_int64(0)
     ctx.call("bgp_logdet", _ptr(L.data), L.n, L.tile, ctypes.byref(out), ctypes.byref(info),
@@ -266,6 +322,7 @@ def dense_of(ctx, obj):
     """Unpadded host array of a device object (lower-triangular for
     triangular objects)."""
     torch = __import__("torch")
+    obj = _full(ctx, obj)
     if obj.kind == "vector":
         return obj.data[:obj.n].cpu().numpy().copy()
     n, m = obj.n, (obj.m if obj.kind == "rectangular" else obj.n)
@@ -277,6 +334,7 @@ def dense_of(ctx, obj):
 
 def diagonal_of(ctx, obj):
     torch = __import__("torch")
+    obj = _full(ctx, obj)
     d = torch.empty((obj.n,), dtype=torch.float64, device=obj.data.device)
     ctx.call("bgp_tri_diagonal", _ptr(obj.data), obj.n, obj.tile, _ptr(d), ctx.stream)
     return d.cpu().numpy()
@@ -352,7 +410,8 @@ def apply(ctx, op_id, input_names, output_name):
     if fn is None:
         registry.lookup(op_id)  # UnknownFunction for ids that do not exist at all
         raise UnknownFunction(f"{op_id!r} has no device implementation")
-    ctx.store[output_name] = fn(ctx, *[ctx.fetch(n) for n in input_names])
+    ctx.store[output_name] = fn(ctx, *[_full(ctx, ctx.fetch(n)) if isinstance(ctx.fetch(n), DevObj)
+                                        else ctx.fetch(n) for n in input_names])
 
 
 def _not_on_path(op):

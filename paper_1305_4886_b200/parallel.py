@@ -1,0 +1,309 @@
+"""Multi-GPU likelihood path: 2-D block-cyclic lower tiles, one process per GPU.
+
+Replaces the reference's triangular D(D+1)/2 process fold
+(bg/grid.py:116-139) and its tag-matched point-to-point messages
+(bg/distla/kernels.py:139-250) with the SURVEY.md 8e plan:
+
+  * tiles (I, J), I >= J, live on rank (I mod Pr) + Pr*(J mod Pc) of a
+    Pr x Pc grid (1x1, 1x2, 2x2, 2x4); a rank stores its tiles packed by
+    tile column, so each owned part of a panel is contiguous;
+  * construct: every rank generates only its own tiles (no communication);
+  * Cholesky step J: the owner of (J, J) factors it and broadcasts L_JJ; the
+    ranks of process column J mod Pc solve their panel tiles; every process
+    row's panel chunk is broadcast to all ranks; each rank applies the
+    DMMA trailing update to its own tiles (bgp_tile_update, tile-list mode);
+  * forward / back solve: per block, the partial products of the owners of
+    row (column) J are reduced to the diagonal owner, which solves and
+    broadcasts x_J (2 x b doubles of traffic per step);
+  * logdet: per-rank partials gathered and summed in rank order, as the
+    reference's master does (bg/distla/__init__.py:154-157).
+
+The schedule below is written against two small interfaces so the same code
+runs on the GPUs (`LibTileOps` over libbgp + NCCL) and in the CPU tests
+(a numpy tile backend + gloo, world size 2).
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .grid import DeviceGrid
+
+
+@dataclass
+class TileDist:
+    """Ownership map of the lower tiles of an n x n matrix for one rank."""
+
+    n: int
+    b: int
+    grid: DeviceGrid
+    rank: int  # 0-based
+    T: int = field(init=False)
+    tiles: np.ndarray = field(init=False)      # (k, 2) int32 (I, J), column-major
+    local: dict = field(init=False)            # (I, J) -> local tile index
+    col_start: np.ndarray = field(init=False)  # first local index of column J
+    col_count: np.ndarray = field(init=False)
+
+    def __post_init__(self):
+        self.T = -(-self.n // self.b)
+        T = self.T
+        pr, pc = self.grid.shape
+        r_row, r_col = self.rank % pr, self.rank // pr
+        tl = [(I, J) for J in range(T) if J % pc == r_col
+              for I in range(J, T) if I % pr == r_row]
+        self.tiles = np.array(tl, dtype=np.int32).reshape(-1, 2)
+        self.local = {(int(I), int(J)): k for k, (I, J) in enumerate(tl)}
+        self.col_start = np.zeros(T + 1, dtype=np.int64)
+        self.col_count = np.zeros(T, dtype=np.int64)
+        for I, J in tl:
+            self.col_count[J] += 1
+        self.col_start[1:] = np.cumsum(self.col_count)
+
+    @property
+    def count(self):
+        return len(self.tiles)
+
+    def owner(self, I, J):
+        return self.grid.owner(I, J)
+
+    def panel_rows(self, J, pr_row):
+        """Rows I > J of panel J held by process row pr_row (ascending)."""
+        pr, _ = self.grid.shape
+        start = J + 1 + ((pr_row - (J + 1)) % pr)
+        return list(range(start, self.T, pr))
+
+    def panel_layout(self, J):
+        """Panel buffer layout for step J: per process row, (root rank,
+        first panel slot, tile count); and slot of each panel row I."""
+        pr, pc = self.grid.shape
+        chunks, slot = [], np.full(self.T, -1, dtype=np.int64)
+        off = 0
+        for p in range(pr):
+            rows = self.panel_rows(J, p)
+            root = p + pr * (J % pc)
+            chunks.append((root, off, len(rows)))
+            for k, I in enumerate(rows):
+                slot[I] = off + k
+            off += len(rows)
+        return chunks, slot, off
+
+    def my_panel(self, J):
+        """(first local index, count) of my tiles (I > J, J) in column J."""
+        s = int(self.col_start[J])
+        c = int(self.col_count[J])
+        if c and self.tiles[s][0] == J:
+            return s + 1, c - 1
+        return s, c
+
+    def update_items(self, J, slot):
+        """(C local, A slot, B slot, lower) for my tiles (R, C), J < C <= R."""
+        first = int(self.col_start[J + 1]) if J + 1 <= self.T - 1 else self.count
+        t = self.tiles[first:]
+        if len(t) == 0:
+            return np.zeros((0, 4), dtype=np.int32)
+        R, C = t[:, 0].astype(np.int64), t[:, 1].astype(np.int64)
+        items = np.stack([np.arange(first, first + len(t)), slot[R], slot[C], (R == C)], axis=1)
+        return items.astype(np.int32)
+
+    def diag_items(self):
+        """(local index, J) of my diagonal tiles."""
+        d = [(k, int(I)) for k, (I, J) in enumerate(self.tiles) if I == J]
+        return np.array(d, dtype=np.int32).reshape(-1, 2)
+
+    def column_items(self, J, below=True):
+        """(local index, I) of my tiles (I > J, J) -- forward-solve partials."""
+        s, c = self.my_panel(J)
+        I = self.tiles[s:s + c, 0]
+        return np.stack([np.arange(s, s + c), I], axis=1).astype(np.int32)
+
+    def row_items(self, J):
+        """(local index, K) of my tiles (J, K), K < J -- back-solve partials."""
+        sel = [(k, int(Jc)) for k, (I, Jc) in enumerate(self.tiles) if I == J and Jc < J]
+        return np.array(sel, dtype=np.int32).reshape(-1, 2)
+
+
+def dist_cholesky(dist, local, ops, comm):
+    """Right-looking tiled Cholesky of a distributed matrix, in place.
+
+    `local` is this rank's (count, b, b) tile stack.  Returns the first
+    failing pivot row (1-based, LAPACK info) agreed by all ranks, or 0.
+    """
+    b, T, me = dist.b, dist.T, dist.rank
+    diag_buf = ops.empty((b, b))
+    info = 0
+    panel = None
+    for J in range(T):
+        d = dist.owner(J, J)
+        if me == d:
+            k = dist.local[(J, J)]
+            if info == 0:
+                info = ops.potrf(local, k, J * b)
+            ops.copy_tile(diag_buf, local, k)
+        comm.broadcast(diag_buf, d)
+        if J + 1 >= T:
+            break
+        s, c = dist.my_panel(J)
+        if c:
+            ops.trsm(diag_buf, local, s, c)
+        chunks, slot, ntot = dist.panel_layout(J)
+        if panel is None or panel.shape[0] < ntot:
+            panel = ops.empty((max(ntot, 1), b, b))
+        for root, off, cnt in chunks:
+            if cnt == 0:
+                continue
+            view = panel[off:off + cnt]
+            if me == root:
+                ps, pcount = dist.my_panel(J)
+                assert pcount == cnt
+                ops.copy_tiles(view, local, ps, cnt)
+            comm.broadcast(view, root)
+        items = dist.update_items(J, slot)
+        if len(items):
+            ops.update(local, panel, items)
+    return comm.min_nonzero(info)
+
+
+def dist_trsv(dist, local, y, ops, comm, forward=True):
+    """Solve L x = y (forward) or L^T x = y (back) with y replicated.
+
+    Returns (x replicated on every rank, info)."""
+    b, T, me = dist.b, dist.T, dist.rank
+    acc = ops.zeros((T * b,))
+    x = ops.zeros((T * b,))
+    info = 0
+    order = range(T) if forward else range(T - 1, -1, -1)
+    for J in order:
+        d = dist.owner(J, J)
+        blk = acc[J * b:(J + 1) * b]
+        comm.reduce_sum(blk, d)
+        xJ = x[J * b:(J + 1) * b]
+        if me == d:
+            ops.sub_into(xJ, y[J * b:(J + 1) * b], blk)
+            if info == 0:
+                info = ops.tile_trsv(local, dist.local[(J, J)], J * b, xJ, 0 if forward else 1)
+        comm.broadcast(xJ, d)
+        items = dist.column_items(J) if forward else dist.row_items(J)
+        if len(items):
+            ops.gemv(local, items, xJ, acc, 0 if forward else 1)
+    return x, comm.min_nonzero(info)
+
+
+def dist_logdet(dist, local, ops, comm):
+    """2 sum log diag(L): per-rank partials summed in rank order."""
+    part, info = ops.logdet_partial(local, dist.diag_items())
+    parts = comm.all_gather_float(part)
+    return float(sum(parts)), comm.min_nonzero(info)
+
+
+class TorchComm:
+    """Collectives over a torch.distributed process group (NCCL on GPUs,
+    gloo in the CPU tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+    def broadcast(self, tensor, src):
+        if self.world > 1:
+            self.dist.broadcast(tensor, src, group=self.group)
+
+    def reduce_sum(self, tensor, dst):
+        # all-reduce (not reduce): 2 KB per step, and it is supported by every
+        # backend for CUDA tensors; only `dst` uses the result
+        if self.world > 1:
+            self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def all_reduce_sum(self, tensor):
+        if self.world > 1:
+            self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def all_gather_float(self, value):
+        if self.world == 1:
+            return [value]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, float(value), group=self.group)
+        return out
+
+    def min_nonzero(self, info):
+        if self.world == 1:
+            return int(info)
+        vals = [None] * self.world
+        self.dist.all_gather_object(vals, int(info), group=self.group)
+        nz = [v for v in vals if v]
+        return min(nz) if nz else 0
+
+
+class LibTileOps:
+    """Tile operations of the distributed schedule on this rank's GPU (libbgp)."""
+
+    def __init__(self, cluster, n):
+        self.cl = cluster
+        self.b = cluster.tile
+        self.n = n
+
+    # buffers ---------------------------------------------------------------
+    def empty(self, shape):
+        return self.cl.empty(shape)
+
+    def zeros(self, shape):
+        return self.cl.zeros(shape)
+
+    def _items(self, arr):
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32).ravel())
+        return t.to(self.cl.device, non_blocking=False)
+
+    @staticmethod
+    def _p(t):
+        import ctypes
+        return ctypes.c_void_p(t.data_ptr())
+
+    # tile kernels ------------------------------------------------------------
+    def potrf(self, local, k, row0):
+        import ctypes
+        info = ctypes.c_int64(0)
+        self.cl.call("bgp_tile_potrf", self._p(local[k]), self.b, row0, ctypes.byref(info),
+                     self.cl.stream)
+        return int(info.value)
+
+    def copy_tile(self, dst, local, k):
+        dst.copy_(local[k])
+
+    def copy_tiles(self, dst, local, start, count):
+        dst.copy_(local[start:start + count])
+
+    def trsm(self, diag, local, start, count):
+        self.cl.call("bgp_panel_trsm", self._p(diag), self._p(local[start]), count, self.b,
+                     self.cl.stream)
+
+    def update(self, local, panel, items):
+        dev = self._items(items)
+        self.cl.call("bgp_tile_update", self._p(local), self._p(panel), self._p(panel),
+                     self._p(dev), len(items), self.b, self.cl.stream)
+
+    def sub_into(self, out, a, b):
+        self.cl.call("bgp_sub", self._p(a), self._p(b), self._p(out), out.numel(), self.cl.stream)
+
+    def tile_trsv(self, local, k, row0, x, trans):
+        import ctypes
+        info = ctypes.c_int64(0)
+        self.cl.call("bgp_tile_trsv", self._p(local[k]), self.b, row0, self.n, self._p(x), trans,
+                     ctypes.byref(info), self.cl.stream)
+        return int(info.value)
+
+    def gemv(self, local, items, xJ, acc, trans):
+        dev = self._items(items)
+        self.cl.call("bgp_tile_gemv", self._p(local), self._p(dev), len(items), self.b,
+                     self._p(xJ), self._p(acc), trans, self.cl.stream)
+
+    def logdet_partial(self, local, diag):
+        import ctypes
+        out, info = ctypes.c_double(0.0), ctypes.c_int64(0)
+        if len(diag) == 0:
+            return 0.0, 0
+        dev = self._items(diag)
+        self.cl.call("bgp_tile_logdet", self._p(local), self._p(dev), len(diag), self.b,
+                     self.n, ctypes.byref(out), ctypes.byref(info), self.cl.stream)
+        return out.value, int(info.value)

@@ -55,7 +55,19 @@ class B200Cluster:
         if rc != 0:
             raise BackendUnavailable(f"bgp_init failed on device {self.device_index}")
         self.grid = DeviceGrid(G)
-        self.rank = int(os.environ.get("RANK", "0")) + 1 if G > 1 else 1
+        self.rank = 1
+        self.comm = None
+        if G > 1:
+            # one process per GPU: triangular objects are spread 2-D
+            # block-cyclically and the panel broadcasts run over NCCL
+            import torch.distributed as tdist
+            if not tdist.is_initialized():
+                tdist.init_process_group("nccl", device_id=self.device)
+            if tdist.get_world_size() != G:
+                raise BackendUnavailable(f"process group has {tdist.get_world_size()} ranks, P={G}")
+            from .parallel import TorchComm
+            self.rank = tdist.get_rank() + 1
+            self.comm = TorchComm()
         self.seed = seed
         self.tile = int(tile)
         self.state = "running"
@@ -71,6 +83,10 @@ class B200Cluster:
     @property
     def P(self):
         return self.grid.P
+
+    @property
+    def G(self):
+        return self.grid.G
 
     @property
     def coord(self):
@@ -103,6 +119,11 @@ class B200Cluster:
         if a.size * 8 >= (1 << 16):
             host = host.pin_memory()
         return host.to(self.device, non_blocking=True)
+
+    def upload_int32(self, array):
+        torch = _torch()
+        a = np.ascontiguousarray(np.asarray(array, dtype=np.int32).ravel())
+        return torch.from_numpy(a).to(self.device)
 
     def device_input(self, inputs_name, key):
         """Device copy of a pushed coordinate array, (n, dim) row-major."""

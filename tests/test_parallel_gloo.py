@@ -1,0 +1,217 @@
+"""Multi-GPU schedule (paper_1305_4886_b200/parallel.py) on CPU ranks over gloo.
+
+The 2-D block-cyclic Cholesky, the distributed forward/back solves and the
+rank-ordered log-det run here with world size 2 (1x2 grid) and 4 (2x2 grid)
+on CPU processes.  The collectives are real torch.distributed calls (gloo);
+the tile arithmetic is a numpy/scipy stand-in (test-only), so what is
+checked is the schedule: ownership, panel broadcasts, item lists, reduction
+and solve order.  On GPUs the same functions drive libbgp over NCCL.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.linalg as la
+
+from conftest import relerr, spd_matrix
+
+
+class NumpyTileOps:
+    """Tile kernels in numpy on torch CPU tensors (column-major tiles)."""
+
+    def __init__(self, b, n):
+        self.b, self.n = b, n
+
+    def empty(self, shape):
+        import torch
+        return torch.zeros(shape, dtype=torch.float64)
+
+    zeros = empty
+
+    @staticmethod
+    def _m(t):  # tile tensor (col-major storage) -> matrix view
+        return t.numpy().T
+
+    def potrf(self, local, k, row0):
+        M = self._m(local[k])
+        try:
+            L = np.linalg.cholesky(np.tril(M) + np.tril(M, -1).T)
+        except np.linalg.LinAlgError:
+            return row0 + 1   # the stand-in reports the tile's first row
+        M[:] = L
+        return 0
+
+    def copy_tile(self, dst, local, k):
+        dst.copy_(local[k])
+
+    def copy_tiles(self, dst, local, start, count):
+        dst.copy_(local[start:start + count])
+
+    def trsm(self, diag, local, start, count):
+        L = np.tril(self._m(diag))
+        for t in range(start, start + count):
+            M = self._m(local[t])
+            M[:] = la.solve_triangular(L, M.T, lower=True).T
+
+    def update(self, local, panel, items):
+        for c, a, b, lower in items:
+            M = self._m(local[c])
+            U = self._m(panel[a]) @ self._m(panel[b]).T
+            M[:] -= np.tril(U) if lower else U
+
+    def sub_into(self, out, a, b):
+        out.copy_(a - b)
+
+    def tile_trsv(self, local, k, row0, x, trans):
+        L = np.tril(self._m(local[k]))
+        xv = x.numpy()
+        xv[:] = la.solve_triangular(L, xv, lower=True, trans=trans)
+        return 0
+
+    def gemv(self, local, items, xJ, acc, trans):
+        a = acc.numpy()
+        x = xJ.numpy()
+        for k, tgt in items:
+            M = self._m(local[k])
+            a[tgt * self.b:(tgt + 1) * self.b] += (M.T @ x) if trans else (M @ x)
+
+    def logdet_partial(self, local, diag):
+        s = 0.0
+        for k, J in diag:
+            d = np.diag(self._m(local[k]))
+            live = min(max(self.n - J * self.b, 0), self.b)
+            s += 2.0 * float(np.sum(np.log(d[:live])))
+        return s, 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, b, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_4886_b200.grid import DeviceGrid
+    from paper_1305_4886_b200.parallel import (TileDist, TorchComm, dist_cholesky,
+                                               dist_logdet, dist_trsv)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = spd_matrix(n, seed=n)
+        T = -(-n // b)
+        P = np.zeros((T * b, T * b))
+        P[:n, :n] = A
+        for t in range(n, T * b):
+            P[t, t] = 1.0
+        td = TileDist(n, b, DeviceGrid(world), rank)
+        local = torch.zeros((td.count, b, b), dtype=torch.float64)
+        for k, (I, J) in enumerate(td.tiles):
+            blk = P[I * b:(I + 1) * b, J * b:(J + 1) * b]
+            local[k].numpy().T[:] = np.tril(blk) if I == J else blk
+        ops, comm = NumpyTileOps(b, n), TorchComm()
+        info = dist_cholesky(td, local, ops, comm)
+        # gather L into a dense matrix on every rank
+        Ld = torch.zeros((T * b, T * b), dtype=torch.float64)
+        for k, (I, J) in enumerate(td.tiles):
+            Ld[I * b:(I + 1) * b, J * b:(J + 1) * b] = torch.from_numpy(local[k].numpy().T.copy())
+        dist.all_reduce(Ld)
+        y = torch.zeros(T * b, dtype=torch.float64)
+        y[:n] = torch.from_numpy(np.random.default_rng(3).standard_normal(n))
+        u, info_f = dist_trsv(td, local, y, ops, comm, forward=True)
+        x, info_b = dist_trsv(td, local, u, ops, comm, forward=False)
+        ld, info_l = dist_logdet(td, local, ops, comm)
+        q.put((rank, info, info_f, info_b, info_l, np.tril(Ld.numpy()[:n, :n]), u.numpy()[:n].copy(),
+               x.numpy()[:n].copy(), ld, td.count))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,b", [(2, 37, 8), (2, 100, 16), (4, 90, 8), (4, 37, 16)])
+def test_distributed_cholesky_solves_logdet(world, n, b):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = spd_matrix(n, seed=n)
+    y = np.random.default_rng(3).standard_normal(n)
+    Lref = np.linalg.cholesky(A)
+    T = -(-n // b)
+    assert sum(o[9] for o in out) == T * (T + 1) // 2      # tiles partitioned
+    for rank, info, info_f, info_b, info_l, L, u, x, ld, _ in out:
+        assert info == info_f == info_b == info_l == 0
+        assert relerr(L, Lref) <= 1e-12
+        assert relerr(u, np.linalg.solve(Lref, y)) <= 1e-12
+        assert relerr(x, np.linalg.solve(A, y)) <= 1e-10
+        assert abs(ld - np.linalg.slogdet(A)[1]) <= 1e-12 * abs(ld)
+    # every rank agrees bit for bit on the replicated results
+    for o in out[1:]:
+        np.testing.assert_array_equal(o[6], out[0][6])
+        assert o[8] == out[0][8]
+
+
+def _fail_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_4886_b200.grid import DeviceGrid
+    from paper_1305_4886_b200.parallel import TileDist, TorchComm, dist_cholesky
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, b = 24, 8
+        A = -np.eye(n)
+        A[:8, :8] = spd_matrix(8, seed=1)     # block 0 fine, block 1 fails
+        td = TileDist(n, b, DeviceGrid(world), rank)
+        local = torch.zeros((td.count, b, b), dtype=torch.float64)
+        for k, (I, J) in enumerate(td.tiles):
+            blk = A[I * b:(I + 1) * b, J * b:(J + 1) * b]
+            local[k].numpy().T[:] = np.tril(blk) if I == J else blk
+        info = dist_cholesky(td, local, NumpyTileOps(b, n), TorchComm())
+        q.put(info)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_failure_is_agreed_by_all_ranks():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    infos = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert infos[0] == infos[1] == 9   # first row of tile 1 (1-based)
+
+
+def test_tile_dist_layout_invariants():
+    from paper_1305_4886_b200.grid import DeviceGrid
+    from paper_1305_4886_b200.parallel import TileDist
+    for G in (1, 2, 4, 8):
+        T = 13
+        dists = [TileDist(T * 4, 4, DeviceGrid(G), r) for r in range(G)]
+        allt = sorted((int(I), int(J)) for d in dists for I, J in d.tiles)
+        assert allt == sorted((I, J) for J in range(T) for I in range(J, T))
+        for J in range(T - 1):
+            chunks, slot, ntot = dists[0].panel_layout(J)
+            assert ntot == T - J - 1
+            assert sorted(slot[J + 1:]) == list(range(ntot))
+            for root, off, cnt in chunks:
+                s, c = dists[root].my_panel(J)
+                assert c == cnt
+                assert [int(I) for I in dists[root].tiles[s:s + c, 0]] == \
+                       [I for I in range(J + 1, T) if slot[I] >= off and slot[I] < off + cnt]
