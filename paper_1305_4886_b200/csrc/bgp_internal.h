@@ -68,7 +68,7 @@ int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
-                      int trans, cudaStream_t s);
+                      int trans, cudaStream_t s, bool check_info = true);
 
 // DMMA/TMA GEMM problems
 enum GemmMode { GEMM_CHOL_TRAIL = 0, GEMM_RECT_TRAIL = 1, GEMM_SYRK_RECT = 2, GEMM_LIST = 3 };
@@ -82,6 +82,7 @@ struct GemmProblem {
   int64_t count;  // GEMM_LIST: number of (C, A, B, lower) tuples
   const int32_t* items;
   double alpha, beta;  // D = beta*C + alpha*sum(A B^T)
+  bool check_info;     // skip the launch when ctx->d_info records a failure
 };
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s);

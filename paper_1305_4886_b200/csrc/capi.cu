@@ -219,6 +219,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
       p.J = J;
       p.alpha = -1.0;
       p.beta = 1.0;
+      p.check_info = true;
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
       mark();
     }
@@ -305,6 +306,7 @@ int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* B
       p.Tn = T;
       p.alpha = -1.0;
       p.beta = 1.0;
+      p.check_info = true;
       if ((rc = launch_gemm(ctx, p, Bt, Bt, nV, L, nL, nV, s))) return rc;
     }
   }
@@ -441,9 +443,11 @@ int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, in
   int rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, per_tile * sizeof(double));
   if (rc) return rc;
   // the diagonal tile passed here is a standalone factored tile: invert its
-  // 32x32 diagonal blocks (T = 1 packed triangle)
+  // 32x32 diagonal blocks (T = 1 packed triangle).  Tile-level calls never
+  // skip on a recorded status: the caller owns the failure protocol.
+  if ((rc = reset_info(ctx, s))) return rc;
   if ((rc = launch_diag_inv(ctx, Ld, 1, tile, tile, ctx->d_dinv, s))) return rc;
-  return launch_panel_trsm(ctx, Ld, ctx->d_dinv, A, count, tile, 0, s);
+  return launch_panel_trsm(ctx, Ld, ctx->d_dinv, A, count, tile, 0, s, false);
 }
 
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase, const int32_t* triples,
@@ -457,6 +461,7 @@ int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase, const dou
   p.items = triples;
   p.alpha = -1.0;
   p.beta = 1.0;
+  p.check_info = false;
   // tensor-map extents: the caller's bases are only addressed through the
   // listed indices; a generous bound keeps the maps valid
   const int64_t big = (int64_t)1 << 30;

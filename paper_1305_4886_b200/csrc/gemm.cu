@@ -397,7 +397,8 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
   }
   const int64_t slots = ctx->num_sms;
   const int64_t grid = items < slots ? items : slots;
-  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mC, p, ctx->d_info);
+  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mC, p,
+                                                                  p.check_info ? ctx->d_info : nullptr);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");
 }

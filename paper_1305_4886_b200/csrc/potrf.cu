@@ -274,7 +274,7 @@ int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* 
 }
 
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
-                      int trans, cudaStream_t s) {
+                      int trans, cudaStream_t s, bool check_info) {
   if (count <= 0) return BGP_OK;
   (void)trans;
   const size_t smem = ((size_t)b * TRSM_R + TRSM_CH * 33 + NB * 33) * sizeof(double);
@@ -284,7 +284,8 @@ int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A,
     attr_done = true;
   }
   const int64_t grid = count * (b / TRSM_R);
-  panel_trsm_kernel<<<(unsigned)grid, TRSM_THREADS, smem, s>>>(Ld, dinv, A, b, ctx->d_info);
+  panel_trsm_kernel<<<(unsigned)grid, TRSM_THREADS, smem, s>>>(Ld, dinv, A, b,
+                                                                      check_info ? ctx->d_info : nullptr);
   ctx->launches++;
   return check_launch(ctx, "panel_trsm");
 }

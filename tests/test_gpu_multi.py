@@ -82,7 +82,20 @@ def test_multi_rank_path_on_one_gpu(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in range(world))
+    res = {}
+    import queue
+    import time
+    t0 = time.time()
+    while len(res) < world:
+        try:
+            rank, out = q.get(timeout=2)
+            res[rank] = out
+        except queue.Empty:
+            dead = [p for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.time() - t0 > 400:
+                for p in procs:
+                    p.kill()
+                pytest.fail(f"worker failed (exit codes {[p.exitcode for p in procs]})")
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
