@@ -55,39 +55,42 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (*(volatile unsigned long long*)info != 0ull) return;  // an earlier step failed
+  if (info && *(volatile unsigned long long*)info != 0ull) return;  // an earlier step failed
   if (tid == 0) s_fail = 0;
   __syncthreads();
   const int nbk = b / NB;
+  const int q = lane >> 2, s4 = lane & 3;
   for (int kb = 0; kb < nbk; ++kb) {
     const int c0 = kb * NB;
-    // (1) factor the 32x32 diagonal block (rows/cols c0..c0+31)
+    // (1) factor the 32x32 diagonal block: warp 0, lane = row held in
+    // registers; column j is exchanged through shared memory (no shuffles,
+    // so the warp never takes the divergent-shuffle path)
     if (warp == 0) {
+      __shared__ double col[NB];
       double a[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) a[j] = (j <= lane) ? A[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
-      int failj = -1;
+      unsigned failmask = 0u;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        if (failj < 0) {
-          const double piv = __shfl_sync(FULL, a[j], j);
-          if (!(piv > 0.0)) {
-            failj = j;
-          } else {
-            const double ljj = sqrt(piv);
-            const double rinv = 1.0 / ljj;
-            a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
+        if (lane == j) col[j] = a[j];
+        __syncwarp();
+        const double piv = col[j];
+        failmask |= (piv > 0.0) ? 0u : (1u << j);
+        const double ljj = sqrt(piv > 0.0 ? piv : 1.0);
+        const double rinv = 1.0 / ljj;
+        a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
+        __syncwarp();
+        col[lane] = a[j];  // column j of L (rows < j hold 0)
+        __syncwarp();
 #pragma unroll
-            for (int c = j + 1; c < NB; ++c) {
-              const double lcj = __shfl_sync(FULL, a[j], c);
-              if (lane >= c) a[c] = fma(-a[j], lcj, a[c]);
-            }
-          }
-        }
+        for (int c = j + 1; c < NB; ++c)
+          if (lane >= c) a[c] = fma(-a[j], col[c], a[c]);
+        __syncwarp();
       }
-      if (failj >= 0) {
+      if (failmask) {
         if (lane == 0) {
-          set_info(info, row0 + c0 + failj + 1);
+          if (info) set_info(info, row0 + c0 + __ffs(failmask));
           s_fail = 1;
         }
       } else {
@@ -100,50 +103,76 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
     }
     __syncthreads();
     if (s_fail) return;
-    // (1b) invert it (warp 0); the inverse feeds the sub-panel solve and the
-    // panel TRSM kernel (global copy)
+    // (1b) invert it (warp 0): feeds the sub-panel solve and panel_trsm
     if (warp == 0) warp_trinv32(D, Dinv_s, dinv ? dinv + (int64_t)kb * NB * NB : nullptr, lane);
     __syncthreads();
     const int rest = b - c0 - NB;  // rows below the diagonal block
     if (rest <= 0) break;
-    // (2) sub-panel X = A[c0+32:, c0:c0+32] Dinv^T  (in place + smem copy)
+    // (2) sub-panel X = A[c0+32:, c0:c0+32] Dinv^T (in place + smem copy);
+    // Dinv is lower triangular with explicit zeros, so every dot is 32 long
     for (int r = tid; r < rest; r += POTRF_THREADS) {
       const int64_t gi = c0 + NB + r;
       double av[NB];
 #pragma unroll
       for (int k = 0; k < NB; ++k) av[k] = A[(int64_t)(c0 + k) * b + gi];
-#pragma unroll
+#pragma unroll 2
       for (int j = 0; j < NB; ++j) {
-        double s = 0.0;
+        const double* dj = Dinv_s + j * 33;
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int k = 0; k <= j; ++k) s = fma(av[k], Dinv_s[j * 33 + k], s);
-        A[(int64_t)(c0 + j) * b + gi] = s;
-        P[r * PLD + j] = s;
+        for (int k = 0; k < NB; k += 2) {
+          s0 = fma(av[k], dj[k], s0);
+          s1 = fma(av[k + 1], dj[k + 1], s1);
+        }
+        const double x = s0 + s1;
+        A[(int64_t)(c0 + j) * b + gi] = x;
+        P[r * PLD + j] = x;
       }
     }
     __syncthreads();
-    // (3) in-tile trailing update: A[i][j] -= sum_k X[i][k] X[j][k], rows/cols
-    // >= c0+32, lower triangle only, 8x8 DMMA blocks
+    // (3) in-tile trailing update A[i][j] -= sum_k X[i][k] X[j][k] for rows /
+    // cols >= c0+32 (lower triangle), 8x8 DMMA blocks, 4 blocks per warp
+    // iteration so the C-fragment loads overlap
     const int nb8 = rest / 8;
     const int nblk = nb8 * (nb8 + 1) / 2;
-    const int q = lane >> 2, s4 = lane & 3;
-    for (int blk = warp; blk < nblk; blk += POTRF_THREADS / 32) {
-      // decode blk -> (ib >= jb), row-major over the lower triangle
-      int ib = (int)((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
-      while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
-      while (ib * (ib + 1) / 2 > blk) --ib;
-      const int jb = blk - ib * (ib + 1) / 2;
-      const int64_t gr = c0 + NB + ib * 8 + q;
-      const int64_t gc = c0 + NB + jb * 8 + 2 * s4;
-      double c0v = A[gc * b + gr], c1v = A[(gc + 1) * b + gr];
+    constexpr int U = 4;
+    for (int base = warp * U; base < nblk; base += (POTRF_THREADS / 32) * U) {
+      int ibs[U], jbs[U];
+      double cv[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int blk = base + u;
+        int ib = 0, jb = 0;
+        if (blk < nblk) {
+          ib = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+          while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+          while (ib * (ib + 1) / 2 > blk) --ib;
+          jb = blk - ib * (ib + 1) / 2;
+        }
+        ibs[u] = ib;
+        jbs[u] = jb;
+        const int64_t gr = c0 + NB + ib * 8 + q;
+        const int64_t gc = c0 + NB + jb * 8 + 2 * s4;
+        cv[u][0] = (blk < nblk) ? A[gc * b + gr] : 0.0;
+        cv[u][1] = (blk < nblk) ? A[(gc + 1) * b + gr] : 0.0;
+      }
 #pragma unroll
       for (int kk = 0; kk < NB / 4; ++kk) {
-        const double av = -P[(ib * 8 + q) * PLD + kk * 4 + s4];
-        const double bv = P[(jb * 8 + q) * PLD + kk * 4 + s4];
-        dmma884(c0v, c1v, av, bv);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double av = -P[(ibs[u] * 8 + q) * PLD + kk * 4 + s4];
+          const double bv = P[(jbs[u] * 8 + q) * PLD + kk * 4 + s4];
+          dmma884(cv[u][0], cv[u][1], av, bv);
+        }
       }
-      if (ib != jb || gr >= gc) A[gc * b + gr] = c0v;
-      if (ib != jb || gr >= gc + 1) A[(gc + 1) * b + gr] = c1v;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (base + u >= nblk) continue;
+        const int64_t gr = c0 + NB + ibs[u] * 8 + q;
+        const int64_t gc = c0 + NB + jbs[u] * 8 + 2 * s4;
+        if (ibs[u] != jbs[u] || gr >= gc) A[gc * b + gr] = cv[u][0];
+        if (ibs[u] != jbs[u] || gr >= gc + 1) A[(gc + 1) * b + gr] = cv[u][1];
+      }
     }
     __syncthreads();
   }

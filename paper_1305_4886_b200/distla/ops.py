@@ -202,8 +202,13 @@ def cholesky(ctx, name, out_name):
     info = ctypes.c_int64(0)
     try:
         if obj.dist is not None:
+            import time
             from ..parallel import dist_cholesky
+            ctx.synchronize()
+            t0 = time.perf_counter()
             info.value = dist_cholesky(obj.dist, obj.data, _tile_ops(ctx, obj.n), ctx.comm)
+            ctx.synchronize()
+            ctx.last_cholesky_ms = 1e3 * (time.perf_counter() - t0)
         else:
             ctx.call("bgp_potrf", _ptr(obj.data), obj.n, obj.tile, ctypes.byref(info), ctx.stream)
     except BaseException:

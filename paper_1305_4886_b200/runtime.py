@@ -76,6 +76,7 @@ class B200Cluster:
         self.store = {RUNTIME_OBJECT: {"rank": self.rank, "device": self.device_index,
                                        "G": G, "tile": self.tile, "seed": seed}}
         self._dev_inputs = {}
+        self.last_cholesky_ms = None
         self.events = []
         self.events_enabled = False
 
