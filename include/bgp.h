@@ -132,6 +132,12 @@ int bgp_xprod_self_diag(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
 int bgp_xprod_self(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
                    int tile, double* S, void* stream);
 
+/* y = L x (mode 0, mult_vector, bg/distla/kernels.py:313-343), y = L^T x
+ * (mode 1) or y = C x with C symmetric and stored as its lower triangle
+ * (mode 2, residual probes).  x, y: (device) length ceil(n/b)*b, distinct. */
+int bgp_tri_mv(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+               const double* x, double* y, int mode, void* stream);
+
 /* ---- K3d reductions (bg/distla/kernels.py:493-522, __init__.py:154-162) ----
  * logdet = 2 sum_{i<n} log L_ii (fixed-order tree sum); info = 1-based row
  * of the first non-positive diagonal (SingularDiagonal) or 0. */

@@ -53,6 +53,7 @@ SIGNATURES = {
     "bgp_xprod_mat_vec": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp, _c_dp]),
     "bgp_xprod_self_diag": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp]),
     "bgp_xprod_self": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp]),
+    "bgp_tri_mv": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _c_dp, _int, _c_dp]),
     "bgp_logdet": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(_i64), _c_dp]),
     "bgp_sumsq": (_int, [ctypes.c_void_p, _c_dp, _i64, ctypes.POINTER(ctypes.c_double), _c_dp]),

@@ -90,6 +90,8 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
 int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s);
 int launch_trsm_rect_back(Ctx* ctx, const double* L, int64_t n, int b, double* Bt, int64_t m,
                           cudaStream_t s);
+int launch_tri_mv(Ctx* ctx, const double* L, int64_t n, int b, const double* x, double* y, int trans, int sym,
+                  cudaStream_t s);
 int launch_logdet(Ctx* ctx, const double* L, int64_t n, int b, cudaStream_t s);
 int launch_sumsq(Ctx* ctx, const double* x, int64_t n, cudaStream_t s);
 int launch_rowdot(Ctx* ctx, const double* Vt, int64_t n, int64_t m, int b, const double* u, double* w,

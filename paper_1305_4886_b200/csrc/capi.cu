@@ -341,6 +341,12 @@ int bgp_xprod_self(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m, int ti
   return launch_gemm(ctx, p, S, Vt, nV, Vt, nV, tri_count(Tm), (cudaStream_t)stream);
 }
 
+int bgp_tri_mv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, const double* x, double* y, int mode,
+               void* stream) {
+  if (!valid_tile(tile) || n < 1 || mode < 0 || mode > 2) return BGP_E_ARG;
+  return launch_tri_mv(ctx, L, n, tile, x, y, mode == 1, mode == 2, (cudaStream_t)stream);
+}
+
 int bgp_logdet(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* out, int64_t* info, void* stream) {
   if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

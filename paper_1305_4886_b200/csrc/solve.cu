@@ -177,6 +177,69 @@ int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int tran
 }
 
 // ---------------------------------------------------------------------------
+// y = L x (trans 0) / L^T x (trans 1) / C x for a symmetric C stored as its
+// lower triangle (sym 1); one CTA per row block I, fixed J order, so the
+// result is deterministic.  mult_vector (bg/distla/kernels.py:313-343) and
+// the residual probes of the n = 131,072 checks.
+__global__ void __launch_bounds__(256) tri_mv_kernel(const double* __restrict__ L, int T, int b,
+                                                     const double* __restrict__ x, double* __restrict__ y,
+                                                     int trans, int sym) {
+  __shared__ double xs[512];
+  __shared__ double red[8][512 / 8 + 1];
+  const int I = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double acc0 = 0.0, acc1 = 0.0;  // rows tid, tid + 256
+  // lower part: L_IJ x_J for J <= I (trans 0 / sym)
+  if (!trans || sym) {
+    for (int J = 0; J <= I; ++J) {
+      __syncthreads();
+      for (int i = tid; i < b; i += blockDim.x) xs[i] = x[(int64_t)J * b + i];
+      __syncthreads();
+      const double* tile = L + tri_index(I, J, T) * (int64_t)b * b;
+      for (int i = tid; i < b; i += blockDim.x) {
+        double a = 0.0;
+        for (int k = 0; k < b; ++k) a = fma(tile[(int64_t)k * b + i], xs[k], a);
+        if (i == tid) acc0 += a; else acc1 += a;
+      }
+    }
+  }
+  // transposed part: L_JI^T x_J for J >= I (trans) or J > I (sym, plus the
+  // strict upper half of the diagonal tile)
+  if (trans || sym) {
+    for (int J = I; J < T; ++J) {
+      __syncthreads();
+      for (int i = tid; i < b; i += blockDim.x) xs[i] = x[(int64_t)J * b + i];
+      __syncthreads();
+      const double* tile = L + tri_index(J, I, T) * (int64_t)b * b;
+      // column k of tile (J, I) dotted with x_J -> output row k of block I
+      for (int k = warp; k < b; k += 8) {
+        double a = 0.0;
+        for (int i = lane; i < b; i += 32) {
+          const bool use = (J > I) || (sym ? (i > k) : (i >= k));
+          if (use) a = fma(tile[(int64_t)k * b + i], xs[i], a);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULLM, a, o);
+        if (lane == 0) red[k & 7][k >> 3] = a;
+      }
+      __syncthreads();
+      for (int i = tid; i < b; i += blockDim.x) {
+        if (i == tid) acc0 += red[i & 7][i >> 3]; else acc1 += red[i & 7][i >> 3];
+      }
+    }
+  }
+  for (int i = tid; i < b; i += blockDim.x) y[(int64_t)I * b + i] = (i == tid) ? acc0 : acc1;
+}
+
+int launch_tri_mv(Ctx* ctx, const double* L, int64_t n, int b, const double* x, double* y, int trans, int sym,
+                  cudaStream_t s) {
+  const int T = (int)((n + b - 1) / b);
+  tri_mv_kernel<<<T, 256, 0, s>>>(L, T, b, x, y, trans, sym);
+  ctx->launches++;
+  return check_launch(ctx, "tri_mv");
+}
+
+// ---------------------------------------------------------------------------
 // L^T X = B for a transposed rectangular RHS (off the north-star path: one
 // thread per RHS column, O(n^2) dot-product substitution, in place)
 __global__ void trsm_rect_back_kernel(const double* __restrict__ L, int T, int b, int64_t n,

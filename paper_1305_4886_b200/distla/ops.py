@@ -426,7 +426,19 @@ def _not_on_path(op):
     return fn
 
 
-for _op in ("distla.rnorm", "distla.mult_vector", "distla.mult_rect"):
+@registry.register("distla.mult_vector")
+def mult_vector(ctx, l_name, x_name, out_name):
+    """y = L x (bg/distla/kernels.py:313-343)."""
+    L = _need(ctx, l_name, "triangular")
+    x = _need(ctx, x_name, "vector")
+    if x.n != L.n:
+        raise DimensionMismatch("x does not conform to L")
+    y = ctx.empty(x.data.shape)
+    ctx.call("bgp_tri_mv", _ptr(L.data), L.n, L.tile, _ptr(x.data), _ptr(y), 0, ctx.stream)
+    ctx.store[out_name] = DevObj("vector", x.row_layout, None, x.tile, y)
+
+
+for _op in ("distla.rnorm", "distla.mult_rect"):
     registry.register(_op, _not_on_path(_op))
 for _op in ("sub", "add", "negate"):
     registry.register(_op, _op)
