@@ -138,6 +138,21 @@ int bgp_xprod_self(bgp_ctx_t ctx, const double* Vt, int64_t n, int64_t m,
 int bgp_tri_mv(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
                const double* x, double* y, int mode, void* stream);
 
+/* Y^T = X^T L^T for transposed rectangular X (m x n tiles): Y = L X, the
+ * rectangular mult_chol of simulation (bg/distla/kernels.py:346-381), on the
+ * DMMA GEMM (Yt must not alias Xt). */
+int bgp_trmm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+                  const double* Xt, int64_t m, double* Yt, void* stream);
+/* N(0,1) fill from the rank stream of bg/rng.py:18-28 (Philox4x64-10 keyed by
+ * (seed << 64) + rank, inverse normal CDF), starting `offset` draws into the
+ * stream, in the reference's block order for API block sizes bs_r x bs_c
+ * (bg/distla/kernels.py:78-104).  m = 0: vector of length n (dense); m > 0:
+ * n x m object written as transposed tiles.  Padding entries are untouched
+ * (zero-initialise `out`). */
+int bgp_rnorm(bgp_ctx_t ctx, int64_t n, int64_t m, int64_t bs_r, int64_t bs_c,
+              uint64_t seed, uint64_t rank, uint64_t offset, int tile,
+              double* out, void* stream);
+
 /* ---- K3d reductions (bg/distla/kernels.py:493-522, __init__.py:154-162) ----
  * logdet = 2 sum_{i<n} log L_ii (fixed-order tree sum); info = 1-based row
  * of the first non-positive diagonal (SingularDiagonal) or 0. */

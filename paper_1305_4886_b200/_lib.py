@@ -53,6 +53,9 @@ SIGNATURES = {
     "bgp_xprod_mat_vec": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp, _c_dp]),
     "bgp_xprod_self_diag": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp]),
     "bgp_xprod_self": (_int, [ctypes.c_void_p, _c_dp, _i64, _i64, _int, _c_dp, _c_dp]),
+    "bgp_trmm_rect": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _i64, _c_dp, _c_dp]),
+    "bgp_rnorm": (_int, [ctypes.c_void_p, _i64, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_uint64,
+                         ctypes.c_uint64, _int, _c_dp, _c_dp]),
     "bgp_tri_mv": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _c_dp, _int, _c_dp]),
     "bgp_logdet": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(_i64), _c_dp]),

@@ -71,7 +71,7 @@ int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A,
                       int trans, cudaStream_t s, bool check_info = true);
 
 // DMMA/TMA GEMM problems
-enum GemmMode { GEMM_CHOL_TRAIL = 0, GEMM_RECT_TRAIL = 1, GEMM_SYRK_RECT = 2, GEMM_LIST = 3 };
+enum GemmMode { GEMM_CHOL_TRAIL = 0, GEMM_RECT_TRAIL = 1, GEMM_SYRK_RECT = 2, GEMM_LIST = 3, GEMM_TRMM_RECT = 4 };
 struct GemmProblem {
   int mode;
   int b;
@@ -90,6 +90,8 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
 int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s);
 int launch_trsm_rect_back(Ctx* ctx, const double* L, int64_t n, int b, double* Bt, int64_t m,
                           cudaStream_t s);
+int launch_rnorm(Ctx* ctx, int64_t n, int64_t m, int64_t bs_r, int64_t bs_c, uint64_t seed, uint64_t rank,
+                 uint64_t offset, int b, double* out, cudaStream_t s);
 int launch_tri_mv(Ctx* ctx, const double* L, int64_t n, int b, const double* x, double* y, int trans, int sym,
                   cudaStream_t s);
 int launch_logdet(Ctx* ctx, const double* L, int64_t n, int b, cudaStream_t s);

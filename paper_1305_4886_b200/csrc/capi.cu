@@ -347,6 +347,29 @@ int bgp_tri_mv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, const double
   return launch_tri_mv(ctx, L, n, tile, x, y, mode == 1, mode == 2, (cudaStream_t)stream);
 }
 
+int bgp_trmm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, const double* Xt, int64_t m, double* Yt,
+                  void* stream) {
+  if (!valid_tile(tile) || n < 1 || m < 1) return BGP_E_ARG;
+  const int b = tile;
+  const int T = (int)((n + b - 1) / b), Tm = (int)((m + b - 1) / b);
+  GemmProblem p{};
+  p.mode = GEMM_TRMM_RECT;
+  p.b = b;
+  p.T = T;
+  p.Tm = Tm;
+  p.Tn = T;
+  p.alpha = 1.0;
+  p.beta = 0.0;
+  const int64_t nV = (int64_t)Tm * T;
+  return launch_gemm(ctx, p, Yt, Xt, nV, L, tri_count(T), nV, (cudaStream_t)stream);
+}
+
+int bgp_rnorm(bgp_ctx_t ctx, int64_t n, int64_t m, int64_t bs_r, int64_t bs_c, uint64_t seed, uint64_t rank,
+              uint64_t offset, int tile, double* out, void* stream) {
+  if (!valid_tile(tile) || n < 1 || m < 0 || bs_r < 1 || bs_c < 1) return BGP_E_ARG;
+  return launch_rnorm(ctx, n, m, bs_r, bs_c, seed, rank, offset, tile, out, (cudaStream_t)stream);
+}
+
 int bgp_logdet(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* out, int64_t* info, void* stream) {
   if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

@@ -56,6 +56,7 @@ constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
 
 struct Item {
   int64_t cTile, aTile0, bTile0;
+  int bTriRow;               // >= 0: B tile for k tile kt is L(bTriRow, kt) (TRMM)
   int64_t aStride, bStride;  // tile-index stride per k tile
   int nkt;                   // number of k tiles
   int mrow0, nrow0;          // row offsets inside the A / B tiles (= C block offsets)
@@ -74,6 +75,8 @@ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
       return (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
     case GEMM_SYRK_RECT:
       return (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
+    case GEMM_TRMM_RECT:
+      return (int64_t)p.Tm * p.T * nblk;
     default:
       return p.count * nblk;
   }
@@ -99,6 +102,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
   it.nkt = 1;
   it.valid = true;
   it.lower = 0;
+  it.bTriRow = -1;
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
       int rr, cc;
@@ -127,6 +131,17 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
       it.aStride = it.bStride = p.Tm;
       it.nkt = p.Tn;
       if (rr == cc) diag_block(it, bi, bj);
+      break;
+    }
+    case GEMM_TRMM_RECT: {  // Y^T(a, I) = sum_{J <= I} X^T(a, J) L(I, J)^T
+      const int a = (int)(t % p.Tm);
+      const int I = (int)(t / p.Tm);
+      it.cTile = (int64_t)I * p.Tm + a;
+      it.aTile0 = a;
+      it.aStride = p.Tm;
+      it.nkt = I + 1;
+      it.bTile0 = 0;
+      it.bTriRow = I;
       break;
     }
     default: {  // GEMM_LIST: (C, A, B, lower) tile-index quadruples
@@ -192,7 +207,8 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
       const int kt = kc / kc_per_tile;
       const int kin = (kc % kc_per_tile) * BK;
       const int at = (int)(it.aTile0 + kt * it.aStride);
-      const int bt = (int)(it.bTile0 + kt * it.bStride);
+      const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, p.T)
+                                     : (int)(it.bTile0 + kt * it.bStride);
       uint8_t* sa = gs.stages + stage * STAGE_BYTES;
       uint8_t* sb = sa + STAGE_A_BYTES;
 #pragma unroll
@@ -377,6 +393,9 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
         break;
       case GEMM_SYRK_RECT:
         items = (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
+        break;
+      case GEMM_TRMM_RECT:
+        items = (int64_t)p.Tm * p.T * nblk;
         break;
       default:
         items = p.count * nblk;

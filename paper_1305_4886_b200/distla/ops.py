@@ -419,13 +419,6 @@ def apply(ctx, op_id, input_names, output_name):
                                         else ctx.fetch(n) for n in input_names])
 
 
-def _not_on_path(op):
-    def fn(ctx, **kwargs):
-        raise UnknownFunction(f"{op!r} is not implemented on the b200 backend yet "
-                              "(simulation is outside the likelihood path)")
-    return fn
-
-
 @registry.register("distla.mult_vector")
 def mult_vector(ctx, l_name, x_name, out_name):
     """y = L x (bg/distla/kernels.py:313-343)."""
@@ -438,8 +431,46 @@ def mult_vector(ctx, l_name, x_name, out_name):
     ctx.store[out_name] = DevObj("vector", x.row_layout, None, x.tile, y)
 
 
-for _op in ("distla.rnorm", "distla.mult_rect"):
-    registry.register(_op, _not_on_path(_op))
+@registry.register("distla.rnorm")
+def construct_rnorm(ctx, name, kind, row_layout, col_layout=None, fill="normal"):
+    """i.i.d. N(0,1) object from this rank's stream (bg/distla/kernels.py:78-104).
+
+    The stream is the reference's (bg/rng.py:18-28): Philox4x64-10 keyed by
+    (seed << 64) + rank, one draw per element of every owned block, padding
+    included, in the reference's block order.  At G = 1 (rank 1, the same
+    API layout as the reference's P = 1) the draws equal the reference's up
+    to the inverse-CDF ulps; with G > 1 every rank draws the rank-1 stream
+    (objects are replicated).  fill="zeros" draws nothing.
+    """
+    from ..errors import StreamsUninitialized
+    if kind not in ("vector", "rectangular"):
+        raise DimensionMismatch(f"rnorm fills vectors or rectangular objects, not {kind!r}")
+    n = row_layout.n
+    m = col_layout.n if kind == "rectangular" else 0
+    out = _alloc(ctx, kind, n, m).zero_()
+    if fill != "zeros":
+        if ctx.seed is None:
+            raise StreamsUninitialized("no master seed installed")
+        bs_r = row_layout.block_size
+        bs_c = col_layout.block_size if kind == "rectangular" else 1
+        nblocks = row_layout.B * (col_layout.B if kind == "rectangular" else 1)
+        ctx.call("bgp_rnorm", n, m, bs_r, bs_c, int(ctx.seed), 1, ctx.stream_pos, ctx.tile,
+                 _ptr(out), ctx.stream)
+        ctx.stream_pos += nblocks * bs_r * bs_c
+    cl = col_layout if kind == "rectangular" else None
+    ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out)
+
+
+@registry.register("distla.mult_rect")
+def mult_rect(ctx, l_name, x_name, out_name):
+    """Y = L X for a rectangular X (bg/distla/kernels.py:346-381), on the DMMA GEMM."""
+    L = _need(ctx, l_name, "triangular")
+    X = _need(ctx, x_name, "rectangular")
+    if X.n != L.n:
+        raise DimensionMismatch("X rows do not conform to L")
+    Y = ctx.empty(X.data.shape)
+    ctx.call("bgp_trmm_rect", _ptr(L.data), L.n, L.tile, _ptr(X.data), X.m, _ptr(Y), ctx.stream)
+    ctx.store[out_name] = DevObj("rectangular", X.row_layout, X.col_layout, X.tile, Y)
 for _op in ("sub", "add", "negate"):
     registry.register(_op, _op)
 

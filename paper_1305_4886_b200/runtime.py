@@ -77,6 +77,7 @@ class B200Cluster:
                                        "G": G, "tile": self.tile, "seed": seed}}
         self._dev_inputs = {}
         self.last_cholesky_ms = None
+        self.stream_pos = 0  # draws consumed from this rank's normal stream
         self.events = []
         self.events_enabled = False
 

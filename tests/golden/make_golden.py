@@ -222,6 +222,26 @@ def main():
     arrays["c2s_y"] = y
     scalars["c2_n2048"] = {"ll": lls}
 
+    # --- simulation (rank streams, bg/rng.py; P = 1) ---------------------
+    from blockgp.rng import RankStream
+    arrays["rng_seed21_rank1"] = RankStream(21, 1).standard_normals(1000)
+    rng = np.random.default_rng(21)
+    X = rng.uniform(0, 1, (60, 2))
+    Xp = rng.uniform(0, 1, (9, 2))
+    theta = np.array([1.3, 0.3, 0.1])
+    y = np.linalg.cholesky(dense_cov("matern-nugget", theta, X, nu=0.5)) @ rng.standard_normal(60)
+    cl = spawn(1, seed=21)
+    try:
+        spec = builtin_spec("matern-nugget", X, Xp, nu=0.5)
+        prob = KrigeProblem(cl, "s", spec, y, theta, m=9)
+        arrays["sim_unc"] = prob.simulate_realizations(4, post=False)
+        arrays["sim_post"] = prob.simulate_realizations(3, post=True)
+        arrays["sim_unc2"] = prob.simulate_realizations(2, post=False)
+    finally:
+        cl.shutdown()
+    arrays.update({"sim_X": X, "sim_Xp": Xp, "sim_y": y})
+    scalars["sim"] = {"seed": 21, "theta": list(theta), "nu": 0.5}
+
     np.savez_compressed(os.path.join(HERE, "golden_small.npz"), **arrays)
     with open(os.path.join(HERE, "golden_scalars.json"), "w") as f:
         json.dump(scalars, f, indent=1, sort_keys=True)
