@@ -187,15 +187,14 @@ __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
 
 __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const CUtensorMap* tmA,
                                               const CUtensorMap* tmB, const CUtensorMap* tmC,
-                                              const GemmProblem& p, int64_t nitems, bool load_c) {
+                                              const GemmProblem& p, int64_t nitems) {
   prefetch_tmap(tmA);
   prefetch_tmap(tmB);
   prefetch_tmap(tmC);
   const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
   const int kc_per_tile = p.b / BK;
   int stage = 0;
-  uint32_t phase = 0, cphase = 0;
+  uint32_t phase = 0;
   for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
        item += (int64_t)GROUPS * gridDim.x) {
     const Item it = gemm_decode(p, item);
@@ -221,23 +220,13 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
         stage = 0;
         phase ^= 1;
       }
-      if (load_c && kc == (nk > 1 ? 1 : 0)) {
-        // C block for the epilogue, once the previous store has drained it
-        mbar_wait(gs.c_empty, cphase ^ 1);
-        mbar_arrive_expect_tx(gs.c_full, CBUF_BYTES);
-#pragma unroll
-        for (int i = 0; i < BM / 16; ++i)
-          tma_load_3d(gs.cbuf + i * CBOX_BYTES, tmC, gs.c_full, it.mrow0 + i * 16, it.nrow0, (int)it.cTile,
-                      pol_stream);
-        cphase ^= 1;
-      }
     }
   }
 }
 
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p, int64_t nitems,
-                                              bool load_c) {
+                                              bool accumulate) {
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
   const bool leader = (gwarp == 0 && lane == 0);
@@ -252,7 +241,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       offB[pp][t] = (uint32_t)(STAGE_A_BYTES + wn * (WN / 16) * 1024) + lane_off(pp, t, q, s4);
     }
   int stage = 0;
-  uint32_t phase = 0, cphase = 0;
+  uint32_t phase = 0;
   bool store_pending = false;
   const uint64_t pol_stream = l2_policy_evict_first();
 
@@ -292,22 +281,14 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         stage = 0;
         phase ^= 1;
       }
-      if (kc == 0 && store_pending && leader) {
-        // previous block's TMA store has to finish reading the C buffer
-        // before the producer may overwrite it
-        tma_store_wait_read0();
-        mbar_arrive(gs.c_empty);
-      }
     }
 
     // ------------------------------- epilogue -------------------------------
-    if (load_c) {
-      mbar_wait(gs.c_full, cphase);
-    } else {
-      if (store_pending && leader) tma_store_wait_read0();
-      named_bar_sync(bar_id, GROUP_WARPS * 32);
-    }
-    cphase ^= 1;
+    // beta = 1 (updates): stage -acc and let the TMA reduce-add it into C in
+    // L2 -- no C load, so no read-modify-write latency on the critical path.
+    // beta = 0 (V^T V, L X): stage acc and TMA-store it.
+    if (store_pending && leader) tma_store_wait_read0();  // staging buffer free
+    named_bar_sync(bar_id, GROUP_WARPS * 32);
     uint8_t* cw = gs.cbuf + wm * (WM / 16) * CBOX_BYTES + wn * WN * 128;
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
@@ -319,10 +300,8 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
           const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
           double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * CBOX_BYTES +
                                                   j * 8 * 128);
-          // alpha/beta are (-1, 1) (updates) or (1, 0) (V^T V): C - acc or acc
-          const double cv = load_c ? *ptr : 0.0;
           const bool keep = it.lower && m < n;  // strict upper triangle stays
-          *ptr = keep ? cv : (load_c ? cv - acc[i][j][e] : acc[i][j][e]);
+          *ptr = keep ? 0.0 : (accumulate ? -acc[i][j][e] : acc[i][j][e]);
         }
       }
     }
@@ -330,8 +309,13 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     named_bar_sync(bar_id, GROUP_WARPS * 32);
     if (leader) {
 #pragma unroll
-      for (int i = 0; i < BM / 16; ++i)
-        tma_store_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile, pol_stream);
+      for (int i = 0; i < BM / 16; ++i) {
+        if (accumulate)
+          tma_reduce_add_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile,
+                            pol_stream);
+        else
+          tma_store_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile, pol_stream);
+      }
       tma_store_commit();
     }
     store_pending = true;
@@ -364,15 +348,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
 
   const int64_t nitems = gemm_num_items(p);
-  const bool load_c = (p.beta != 0.0);
+  const bool accumulate = (p.beta != 0.0);  // (alpha, beta) = (-1, 1) or (1, 0)
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (warp < GROUPS && lane == 0)
-      producer_loop(group_smem(smem, warp), warp, &tmA, &tmB, &tmC, p, nitems, load_c);
+      producer_loop(group_smem(smem, warp), warp, &tmA, &tmB, &tmC, p, nitems);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     const int g = wg - 1;
-    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, load_c);
+    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, accumulate);
   }
 }
 

@@ -27,17 +27,25 @@ constexpr int PLD = 36;       // smem leading dimension of the panel copy (confl
 constexpr int POTRF_THREADS = 256;
 
 // inverse of a lower-triangular 32x32 block held in smem D (ld 33);
-// lane = column of the inverse.  Writes Dinv_s (ld 33) and optionally global
-// (column-major 32x32).
-__device__ __forceinline__ void warp_trinv32(const double* D, double* Dinv_s, double* gout, int lane) {
+// lane = column of the inverse.  rdiag (smem, optional) holds 1/D[i][i]; the
+// dot products use four partial sums to shorten the dependent FMA chain.
+// Writes Dinv_s (ld 33) and optionally global (column-major 32x32).
+__device__ __forceinline__ void warp_trinv32(const double* D, const double* rdiag, double* Dinv_s, double* gout,
+                                             int lane) {
   double x[NB];
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) s = fma(D[i * 33 + k], x[k], s);
-    const double dii = D[i * 33 + i];
-    x[i] = (i == lane) ? 1.0 / dii : ((i > lane) ? -s / dii : 0.0);
+    for (int k = 0; k < i; ++k) {
+      const double t = D[i * 33 + k] * x[k];
+      if ((k & 3) == 0) s0 += t;
+      else if ((k & 3) == 1) s1 += t;
+      else if ((k & 3) == 2) s2 += t;
+      else s3 += t;
+    }
+    const double r = rdiag ? rdiag[i] : 1.0 / D[i * 33 + i];
+    x[i] = (i == lane) ? r : ((i > lane) ? -((s0 + s1) + (s2 + s3)) * r : 0.0);
   }
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
@@ -46,6 +54,96 @@ __device__ __forceinline__ void warp_trinv32(const double* D, double* Dinv_s, do
   }
 }
 
+// Factor the 32x32 diagonal block at (c0, c0) of the tile in global memory
+// (warp-wide; lane = row, column j exchanged through smem `col`), store L in
+// A and D, 1/L_jj in rdiag.  Returns the failure bitmask (warp-uniform).
+__device__ __forceinline__ unsigned warp_potrf32(double* A, int b, int c0, double* D, double* rdiag,
+                                                 double* col, int lane) {
+  double a[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) a[j] = (j <= lane) ? A[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
+  unsigned failmask = 0u;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (lane == j) col[j] = a[j];
+    __syncwarp();
+    const double piv = col[j];
+    failmask |= (piv > 0.0) ? 0u : (1u << j);
+    const double rinv = rsqrt(piv > 0.0 ? piv : 1.0);
+    const double ljj = (piv > 0.0 ? piv : 1.0) * rinv;
+    if (lane == 0) rdiag[j] = rinv;
+    a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
+    __syncwarp();
+    col[lane] = a[j];  // column j of L (rows < j hold 0)
+    __syncwarp();
+#pragma unroll
+    for (int c = j + 1; c < NB; ++c)
+      if (lane >= c) a[c] = fma(-a[j], col[c], a[c]);
+    __syncwarp();
+  }
+  if (!failmask) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      D[lane * 33 + j] = (j <= lane) ? a[j] : 0.0;
+      if (j <= lane) A[(int64_t)(c0 + j) * b + c0 + lane] = a[j];
+    }
+  }
+  __syncwarp();
+  return failmask;
+}
+
+// In-tile trailing update A[i][j] -= sum_k P[i][k] P[j][k] on 8x8 DMMA blocks
+// blk in [first, last) of the lower triangle of the `rest` x `rest` trailing
+// part (row-major block order), handed out round-robin over `nwarps` warps
+// starting at `wid`, four blocks per iteration so the C loads overlap.
+__device__ __forceinline__ void tile_trailing(double* A, int b, int base_rc, const double* P, int first,
+                                              int last, int wid, int nwarps, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+  constexpr int U = 4;
+  for (int base = first + wid * U; base < last; base += nwarps * U) {
+    int ibs[U], jbs[U];
+    double cv[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int blk = base + u;
+      int ib = 0, jb = 0;
+      if (blk < last) {
+        ib = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+        while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+        while (ib * (ib + 1) / 2 > blk) --ib;
+        jb = blk - ib * (ib + 1) / 2;
+      }
+      ibs[u] = ib;
+      jbs[u] = jb;
+      const int64_t gr = base_rc + ib * 8 + q;
+      const int64_t gc = base_rc + jb * 8 + 2 * s4;
+      cv[u][0] = (blk < last) ? A[gc * b + gr] : 0.0;
+      cv[u][1] = (blk < last) ? A[(gc + 1) * b + gr] : 0.0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < NB / 4; ++kk) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double av = -P[(ibs[u] * 8 + q) * PLD + kk * 4 + s4];
+        const double bv = P[(jbs[u] * 8 + q) * PLD + kk * 4 + s4];
+        dmma884(cv[u][0], cv[u][1], av, bv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + u >= last) continue;
+      const int64_t gr = base_rc + ibs[u] * 8 + q;
+      const int64_t gc = base_rc + jbs[u] * 8 + 2 * s4;
+      if (ibs[u] != jbs[u] || gr >= gc) A[gc * b + gr] = cv[u][0];
+      if (ibs[u] != jbs[u] || gr >= gc + 1) A[(gc + 1) * b + gr] = cv[u][1];
+    }
+  }
+}
+
+// Right-looking blocked factorization of one b x b tile with 32-wide
+// sub-panels and a one-block look-ahead inside the tile: while warps 1..7
+// apply sub-panel k's trailing update, warp 0 updates, factors and inverts
+// diagonal block k+1, so the serial 32x32 work overlaps the DMMA update.
 __global__ void __launch_bounds__(POTRF_THREADS, 1)
     tile_potrf_kernel(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
                       unsigned long long* __restrict__ info) {
@@ -53,62 +151,32 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   double* D = sm;                // 32 x 33
   double* Dinv_s = D + NB * 33;  // 32 x 33
   double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
+  __shared__ double rdiag[NB];
+  __shared__ double col[NB];
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (info && *(volatile unsigned long long*)info != 0ull) return;  // an earlier step failed
   if (tid == 0) s_fail = 0;
   __syncthreads();
   const int nbk = b / NB;
-  const int q = lane >> 2, s4 = lane & 3;
-  for (int kb = 0; kb < nbk; ++kb) {
-    const int c0 = kb * NB;
-    // (1) factor the 32x32 diagonal block: warp 0, lane = row held in
-    // registers; column j is exchanged through shared memory (no shuffles,
-    // so the warp never takes the divergent-shuffle path)
-    if (warp == 0) {
-      __shared__ double col[NB];
-      double a[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) a[j] = (j <= lane) ? A[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
-      unsigned failmask = 0u;
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        if (lane == j) col[j] = a[j];
-        __syncwarp();
-        const double piv = col[j];
-        failmask |= (piv > 0.0) ? 0u : (1u << j);
-        const double ljj = sqrt(piv > 0.0 ? piv : 1.0);
-        const double rinv = 1.0 / ljj;
-        a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
-        __syncwarp();
-        col[lane] = a[j];  // column j of L (rows < j hold 0)
-        __syncwarp();
-#pragma unroll
-        for (int c = j + 1; c < NB; ++c)
-          if (lane >= c) a[c] = fma(-a[j], col[c], a[c]);
-        __syncwarp();
+  // prologue: factor + invert diagonal block 0
+  if (warp == 0) {
+    const unsigned fm = warp_potrf32(A, b, 0, D, rdiag, col, lane);
+    if (fm) {
+      if (lane == 0) {
+        if (info) set_info(info, row0 + __ffs(fm));
+        s_fail = 1;
       }
-      if (failmask) {
-        if (lane == 0) {
-          if (info) set_info(info, row0 + c0 + __ffs(failmask));
-          s_fail = 1;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          D[lane * 33 + j] = (j <= lane) ? a[j] : 0.0;
-          if (j <= lane) A[(int64_t)(c0 + j) * b + c0 + lane] = a[j];
-        }
-      }
+    } else {
+      warp_trinv32(D, rdiag, Dinv_s, dinv, lane);
     }
-    __syncthreads();
-    if (s_fail) return;
-    // (1b) invert it (warp 0): feeds the sub-panel solve and panel_trsm
-    if (warp == 0) warp_trinv32(D, Dinv_s, dinv ? dinv + (int64_t)kb * NB * NB : nullptr, lane);
-    __syncthreads();
-    const int rest = b - c0 - NB;  // rows below the diagonal block
-    if (rest <= 0) break;
-    // (2) sub-panel X = A[c0+32:, c0:c0+32] Dinv^T (in place + smem copy);
+  }
+  __syncthreads();
+  if (s_fail) return;
+  for (int kb = 0; kb + 1 < nbk; ++kb) {
+    const int c0 = kb * NB;
+    const int rest = b - c0 - NB;
+    // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy);
     // Dinv is lower triangular with explicit zeros, so every dot is 32 long
     for (int r = tid; r < rest; r += POTRF_THREADS) {
       const int64_t gi = c0 + NB + r;
@@ -130,51 +198,28 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
       }
     }
     __syncthreads();
-    // (3) in-tile trailing update A[i][j] -= sum_k X[i][k] X[j][k] for rows /
-    // cols >= c0+32 (lower triangle), 8x8 DMMA blocks, 4 blocks per warp
-    // iteration so the C-fragment loads overlap
+    // (B) trailing update; the first 10 blocks are diagonal block k+1
     const int nb8 = rest / 8;
     const int nblk = nb8 * (nb8 + 1) / 2;
-    constexpr int U = 4;
-    for (int base = warp * U; base < nblk; base += (POTRF_THREADS / 32) * U) {
-      int ibs[U], jbs[U];
-      double cv[U][2];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int blk = base + u;
-        int ib = 0, jb = 0;
-        if (blk < nblk) {
-          ib = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-          while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
-          while (ib * (ib + 1) / 2 > blk) --ib;
-          jb = blk - ib * (ib + 1) / 2;
+    const int base_rc = c0 + NB;
+    if (warp == 0) {
+      tile_trailing(A, b, base_rc, P, 0, 10, 0, 1, lane);
+      __syncwarp();
+      __threadfence_block();
+      const unsigned fm = warp_potrf32(A, b, base_rc, D, rdiag, col, lane);
+      if (fm) {
+        if (lane == 0) {
+          if (info) set_info(info, row0 + base_rc + __ffs(fm));
+          s_fail = 1;
         }
-        ibs[u] = ib;
-        jbs[u] = jb;
-        const int64_t gr = c0 + NB + ib * 8 + q;
-        const int64_t gc = c0 + NB + jb * 8 + 2 * s4;
-        cv[u][0] = (blk < nblk) ? A[gc * b + gr] : 0.0;
-        cv[u][1] = (blk < nblk) ? A[(gc + 1) * b + gr] : 0.0;
+      } else {
+        warp_trinv32(D, rdiag, Dinv_s, dinv ? dinv + (int64_t)(kb + 1) * NB * NB : nullptr, lane);
       }
-#pragma unroll
-      for (int kk = 0; kk < NB / 4; ++kk) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const double av = -P[(ibs[u] * 8 + q) * PLD + kk * 4 + s4];
-          const double bv = P[(jbs[u] * 8 + q) * PLD + kk * 4 + s4];
-          dmma884(cv[u][0], cv[u][1], av, bv);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (base + u >= nblk) continue;
-        const int64_t gr = c0 + NB + ibs[u] * 8 + q;
-        const int64_t gc = c0 + NB + jbs[u] * 8 + 2 * s4;
-        if (ibs[u] != jbs[u] || gr >= gc) A[gc * b + gr] = cv[u][0];
-        if (ibs[u] != jbs[u] || gr >= gc + 1) A[(gc + 1) * b + gr] = cv[u][1];
-      }
+    } else {
+      tile_trailing(A, b, base_rc, P, 10, nblk, warp - 1, POTRF_THREADS / 32 - 1, lane);
     }
     __syncthreads();
+    if (s_fail) return;
   }
 }
 
@@ -200,7 +245,7 @@ __global__ void diag_inv_kernel(const double* __restrict__ L, int T, int b, int6
     if (lane == 0) set_info(info, (int64_t)J * b + c0 + __ffs(z));
     return;
   }
-  warp_trinv32(D, Dinv_s, dinv + ((int64_t)J * nbk + kb) * NB * NB, lane);
+  warp_trinv32(D, nullptr, Dinv_s, dinv + ((int64_t)J * nbk + kb) * NB * NB, lane);
 }
 
 // X = A L^{-T} (trans = 0) for `count` consecutive b x b tiles.
