@@ -47,8 +47,9 @@ constexpr int MI = WM / 8, NJ = WN / 8;        // 8x8 DMMA tiles per warp
 constexpr int STAGE_A_BYTES = BM * BK * 8;     // 8 KB: 8 boxes of 16x8
 constexpr int STAGE_B_BYTES = BN * BK * 8;     // 4 KB: 4 boxes of 16x8
 constexpr int STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
-constexpr int CBOX_BYTES = 16 * BN * 8;        // 8 KB: box of 16 rows x 64 cols
-constexpr int CBUF_BYTES = BM * BN * 8;        // 64 KB
+constexpr int WBOX_BYTES = 16 * WN * 8;        // 4 KB: epilogue box of 16 rows x 32 cols
+constexpr int WSTAGE_BYTES = WM * WN * 8;      // 16 KB: one warp's epilogue slice
+constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;  // 64 KB per group
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
@@ -229,8 +230,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
                                               bool accumulate) {
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
-  const bool leader = (gwarp == 0 && lane == 0);
-  const int bar_id = 1 + g;
   const int kc_per_tile = p.b / BK;
   uint32_t offA[2][2], offB[2][2];
 #pragma unroll
@@ -284,12 +283,13 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     }
 
     // ------------------------------- epilogue -------------------------------
-    // beta = 1 (updates): stage -acc and let the TMA reduce-add it into C in
-    // L2 -- no C load, so no read-modify-write latency on the critical path.
-    // beta = 0 (V^T V, L X): stage acc and TMA-store it.
-    if (store_pending && leader) tma_store_wait_read0();  // staging buffer free
-    named_bar_sync(bar_id, GROUP_WARPS * 32);
-    uint8_t* cw = gs.cbuf + wm * (WM / 16) * CBOX_BYTES + wn * WN * 128;
+    // Per warp (no group barrier): stage the warp's 64x32 result in its own
+    // 16 KB slice and issue four 16x32 TMA boxes.  beta = 1 (updates): stage
+    // -acc and TMA reduce-add it into C in L2 -- no C load, no read-modify-
+    // write on the critical path.  beta = 0 (V^T V, L X): TMA store of acc.
+    if (store_pending && lane == 0) tma_store_wait_read0();  // slice free again
+    __syncwarp();
+    uint8_t* cw = gs.cbuf + gwarp * WSTAGE_BYTES;
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
       const int m = it.mrow0 + wm * WM + i * 8 + q;
@@ -298,7 +298,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
-          double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * CBOX_BYTES +
+          double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * WBOX_BYTES +
                                                   j * 8 * 128);
           const bool keep = it.lower && m < n;  // strict upper triangle stays
           *ptr = keep ? 0.0 : (accumulate ? -acc[i][j][e] : acc[i][j][e]);
@@ -306,21 +306,21 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       }
     }
     fence_proxy_async_smem();
-    named_bar_sync(bar_id, GROUP_WARPS * 32);
-    if (leader) {
+    __syncwarp();
+    if (lane == 0) {
+      const int r0 = it.mrow0 + wm * WM, c0 = it.nrow0 + wn * WN;
 #pragma unroll
-      for (int i = 0; i < BM / 16; ++i) {
+      for (int i = 0; i < WM / 16; ++i) {
         if (accumulate)
-          tma_reduce_add_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile,
-                            pol_stream);
+          tma_reduce_add_3d(tmC, cw + i * WBOX_BYTES, r0 + i * 16, c0, (int)it.cTile, pol_stream);
         else
-          tma_store_3d(tmC, gs.cbuf + i * CBOX_BYTES, it.mrow0 + i * 16, it.nrow0, (int)it.cTile, pol_stream);
+          tma_store_3d(tmC, cw + i * WBOX_BYTES, r0 + i * 16, c0, (int)it.cTile, pol_stream);
       }
       tma_store_commit();
     }
     store_pending = true;
   }
-  if (leader && store_pending) tma_store_wait_all0();
+  if (lane == 0 && store_pending) tma_store_wait_all0();
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -390,7 +390,7 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
   int rc;
   if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
-  if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, BN, true)) != BGP_OK) return rc;
+  if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
   static int occupancy = -1;
   if (occupancy < 0) {
     cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
