@@ -37,23 +37,30 @@ namespace bgp {
 // The two consumer groups take alternate blocks of the CTA's static schedule
 // and run concurrently, so one group's epilogue overlaps the other group's
 // main loop and the DMMA pipe never drains between blocks.
-constexpr int BM = 128, BN = 64, BK = 8, STAGES = 4;
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
 constexpr int GROUPS = 2;
 constexpr int WARPS_M = 2, WARPS_N = 2;       // per consumer group
 constexpr int GROUP_WARPS = WARPS_M * WARPS_N;
 constexpr int THREADS = 128 * (GROUPS + 1);
 constexpr int WM = 64, WN = 32;                // warp tile
 constexpr int MI = WM / 8, NJ = WN / 8;        // 8x8 DMMA tiles per warp
-constexpr int STAGE_A_BYTES = BM * BK * 8;     // 8 KB: 8 boxes of 16x8
-constexpr int STAGE_B_BYTES = BN * BK * 8;     // 4 KB: 4 boxes of 16x8
+constexpr int BOX_BYTES = 16 * BK * 8;         // 2 KB: operand TMA box of 16 rows x BK k
+constexpr int STAGE_A_BYTES = BM * BK * 8;     // 16 KB: 8 boxes
+constexpr int STAGE_B_BYTES = BN * BK * 8;     // 8 KB: 4 boxes
 constexpr int STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr int WBOX_BYTES = 16 * WN * 8;        // 4 KB: epilogue box of 16 rows x 32 cols
-constexpr int WSTAGE_BYTES = WM * WN * 8;      // 16 KB: one warp's epilogue slice
-constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;  // 64 KB per group
+constexpr int WSTAGE_BYTES = 2 * WBOX_BYTES;   // 8 KB: a warp's epilogue slice (half its tile)
+constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;  // 32 KB per group
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+
+#ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
+constexpr int TRACE_ITEMS = 64;
+__device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][3];
+#endif
 
 struct Item {
   int64_t cTile, aTile0, bTile0;
@@ -158,8 +165,11 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
 }
 
 // Per-lane byte offset of MMA fragment element (row p*8 + q of a 16-row TMA
-// box, k = 2*s4 + t) inside a 128B-swizzled box whose 128-byte lines are k
-// (operands) or n (C buffer): line*128 + (((p<<2) ^ ((q>>1) ^ k)) << 4) + (q&1)*8.
+// box, k = 2*s4 + t, t = 0, 1) inside a 128B-swizzled box whose 128-byte
+// lines are k (operands) or n (C buffer):
+//   line*128 + (((p<<2) ^ ((q>>1) ^ k)) << 4) + (q&1)*8.
+// k-lines 8..15 of a BK = 16 box repeat the swizzle of lines 0..7, so the
+// k4 half-steps t + 2 sit exactly 1024 bytes after half-steps t.
 __device__ __forceinline__ uint32_t lane_off(int p, int t, int q, int s4) {
   const int k = 2 * s4 + t;
   return (uint32_t)(k * 128 + ((((p << 2) ^ ((q >> 1) ^ k)) & 7) << 4) + ((q & 1) << 3));
@@ -170,25 +180,28 @@ struct GroupSmem {
   uint8_t* cbuf;
   uint64_t* full;
   uint64_t* empty;
-  uint64_t* c_full;
-  uint64_t* c_empty;
 };
 
 __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
   GroupSmem gs;
   gs.stages = smem + g * GROUP_BYTES;
   gs.cbuf = gs.stages + STAGES * STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES);
   gs.full = bars;
   gs.empty = bars + STAGES;
-  gs.c_full = bars + 2 * STAGES;
-  gs.c_empty = gs.c_full + 1;
   return gs;
+}
+
+__device__ __forceinline__ uint64_t* stagger_bar(uint8_t* smem) {
+  return reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + GROUPS * 2 * STAGES;
 }
 
 __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const CUtensorMap* tmA,
                                               const CUtensorMap* tmB, const CUtensorMap* tmC,
                                               const GemmProblem& p, int64_t nitems) {
+#ifdef BGP_EXP_NO_BAR
+  return;
+#endif
   prefetch_tmap(tmA);
   prefetch_tmap(tmB);
   prefetch_tmap(tmC);
@@ -203,6 +216,14 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
     const int nk = it.nkt * kc_per_tile;
     for (int kc = 0; kc < nk; ++kc) {
       mbar_wait(&gs.empty[stage], phase ^ 1);
+#ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
+      mbar_arrive(&gs.full[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      continue;
+#endif
       mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
       const int kt = kc / kc_per_tile;
       const int kin = (kc % kc_per_tile) * BK;
@@ -213,10 +234,10 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
       uint8_t* sb = sa + STAGE_A_BYTES;
 #pragma unroll
       for (int i = 0; i < BM / 16; ++i)
-        tma_load_3d(sa + i * 1024, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
+        tma_load_3d(sa + i * BOX_BYTES, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
 #pragma unroll
       for (int i = 0; i < BN / 16; ++i)
-        tma_load_3d(sb + i * 1024, tmB, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
+        tma_load_3d(sb + i * BOX_BYTES, tmB, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
@@ -225,24 +246,118 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
   }
 }
 
+// ld.shared.f64 at a register base plus an immediate; volatile so it keeps
+// its place between the (volatile) DMMAs of the software pipeline below
+template <int OFF>
+__device__ __forceinline__ double lds64(uint32_t base) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(base), "n"(OFF) : "memory");
+  return v;
+}
+
+// one k4 half-step's fragments: A rows i*8.. of the warp tile (box i>>1,
+// row-pair i&1), B columns j*8..
+struct Frag {
+  double a[MI], b[NJ];
+};
+
+template <int H2>  // k lines 8*H2 .. 8*H2 + 7 of the stage
+__device__ __forceinline__ void load_frag(Frag& f, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+  constexpr int K = H2 * 1024;
+  f.a[0] = lds64<K>(a0);
+  f.a[1] = lds64<K>(a1);
+  f.a[2] = lds64<K + BOX_BYTES>(a0);
+  f.a[3] = lds64<K + BOX_BYTES>(a1);
+  f.a[4] = lds64<K + 2 * BOX_BYTES>(a0);
+  f.a[5] = lds64<K + 2 * BOX_BYTES>(a1);
+  f.a[6] = lds64<K + 3 * BOX_BYTES>(a0);
+  f.a[7] = lds64<K + 3 * BOX_BYTES>(a1);
+  f.b[0] = lds64<K>(b0);
+  f.b[1] = lds64<K>(b1);
+  f.b[2] = lds64<K + BOX_BYTES>(b0);
+  f.b[3] = lds64<K + BOX_BYTES>(b1);
+}
+
+__device__ __forceinline__ void mma_frag(double (&acc)[MI][NJ][2], const Frag& f) {
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], f.a[i], f.b[j]);
+}
+
+template <int OFF>
+__device__ __forceinline__ void sts64(uint32_t base, double v) {
+  asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(base), "n"(OFF), "d"(v) : "memory");
+}
+
+// Stage rows ii = 0..3 (of 8-row blocks i = 4r + ii) of the warp's 64x32
+// accumulator tile into its 8 KB epilogue slice: two 16x32 boxes, 128B
+// swizzled like the operands (line = column n).  cb[p][e] are the lane's
+// addresses of (row-pair p, column parity e) in box 0, column block j = 0.
+// NEG stages -acc (integer sign flip, no FP64 instruction); MASK zeroes the
+// strict upper triangle of a diagonal tile (m < n).
+template <int R, bool NEG, bool MASK>
+__device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const uint32_t (&cb)[2][2], int m0,
+                                           int n0) {
+#pragma unroll
+  for (int ii = 0; ii < MI / 2; ++ii) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = acc[R * (MI / 2) + ii][j][e];
+        if (NEG) v = __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull);
+        if (MASK && m0 + ii * 8 < n0 + j * 8 + e) v = 0.0;
+        const uint32_t a = cb[ii & 1][e];
+        switch ((ii >> 1) * NJ + j) {  // immediate offsets: box (ii >> 1), column block j
+          case 0: sts64<0>(a, v); break;
+          case 1: sts64<1024>(a, v); break;
+          case 2: sts64<2048>(a, v); break;
+          case 3: sts64<3072>(a, v); break;
+          case 4: sts64<WBOX_BYTES>(a, v); break;
+          case 5: sts64<WBOX_BYTES + 1024>(a, v); break;
+          case 6: sts64<WBOX_BYTES + 2048>(a, v); break;
+          default: sts64<WBOX_BYTES + 3072>(a, v); break;
+        }
+      }
+    }
+  }
+}
+
+template <bool ACC>
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p, int64_t nitems,
-                                              bool accumulate) {
+                                              uint64_t* stagger) {
+  static_assert(MI == 8 && NJ == 4 && WM / 16 == 4 && WN / 16 == 2, "load_frag assumes a 64x32 warp tile");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
   const int kc_per_tile = p.b / BK;
+  // per-lane shared addresses of the fragments in stage 0 (t = k4 half-step)
+  const uint32_t st0 = smem_u32(gs.stages);
   uint32_t offA[2][2], offB[2][2];
 #pragma unroll
   for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      offA[pp][t] = (uint32_t)(wm * (WM / 16) * 1024) + lane_off(pp, t, q, s4);
-      offB[pp][t] = (uint32_t)(STAGE_A_BYTES + wn * (WN / 16) * 1024) + lane_off(pp, t, q, s4);
+      offA[pp][t] = st0 + (uint32_t)(wm * (WM / 16) * BOX_BYTES) + lane_off(pp, t, q, s4);
+      offB[pp][t] = st0 + (uint32_t)(STAGE_A_BYTES + wn * (WN / 16) * BOX_BYTES) + lane_off(pp, t, q, s4);
     }
+  uint8_t* cw = gs.cbuf + gwarp * WSTAGE_BYTES;
+  uint32_t cbase[2][2];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) cbase[pp][e] = smem_u32(cw) + lane_off(pp, e, q, s4);
   int stage = 0;
   uint32_t phase = 0;
   bool store_pending = false;
   const uint64_t pol_stream = l2_policy_evict_first();
+  // Stagger: every block costs the same, so two groups that start together
+  // would hit their epilogues together and leave the DMMA pipe idle.  Group 1
+  // starts once group 0 is half-way through its first block (group 0 always
+  // arrives exactly once, also when it has no block at all).
+  bool stagger_arrive = (g == 0);
+  if (g == 1) mbar_wait(stagger, 0);
 
   for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
        item += (int64_t)GROUPS * gridDim.x) {
@@ -255,70 +370,127 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kc = 0; kc < nk; ++kc) {
-      mbar_wait(&gs.full[stage], phase);
-      const uint8_t* st = gs.stages + stage * STAGE_BYTES;
-      double af[2][MI], bf[2][NJ];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-          af[t][i] = *reinterpret_cast<const double*>(st + offA[i & 1][t] + (i >> 1) * 1024);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          bf[t][j] = *reinterpret_cast<const double*>(st + offB[j & 1][t] + (j >> 1) * 1024);
+    // Software pipeline over the stage ring.  A stage holds four k4
+    // half-steps (h0..h3); fragments alternate between two register sets, so
+    // the loads of half-step h+1 issue in the DMMA gaps of half-step h.  The
+    // wait for stage s+1 sits before the last half-step of stage s, and
+    // stage s is released once its last DMMA issued (fragments in registers).
+#ifdef BGP_EXP_TRACE
+    const int t_idx = (int)((item - blockIdx.x) / ((int64_t)GROUPS * gridDim.x));
+    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+      g_trace[blockIdx.x][g][t_idx][0] = clock64();
+#endif
+    Frag x, y;
+    uint32_t sb = (uint32_t)stage * STAGE_BYTES;
+#define BGP_LOAD(F, H) load_frag<((H) >> 1)>(F, offA[0][(H) & 1] + sb, offA[1][(H) & 1] + sb, \
+                                             offB[0][(H) & 1] + sb, offB[1][(H) & 1] + sb)
+#ifndef BGP_EXP_NO_BAR
+    mbar_wait(&gs.full[stage], phase);
+#endif
+    BGP_LOAD(x, 0);
+    for (int kc = 0; kc + 1 < nk; ++kc) {
+      const int cur = stage;
+      if (stagger_arrive && kc == (nk >> 1)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stagger);
+        stagger_arrive = false;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&gs.empty[stage]);  // fragments are in registers
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[t][i], bf[t][j]);
+      BGP_LOAD(y, 1);
+      mma_frag(acc, x);
+      BGP_LOAD(x, 2);
+      mma_frag(acc, y);
+      BGP_LOAD(y, 3);
+      mma_frag(acc, x);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
       }
+      sb = (uint32_t)stage * STAGE_BYTES;
+#ifndef BGP_EXP_NO_BAR
+      mbar_wait(&gs.full[stage], phase);
+#endif
+      BGP_LOAD(x, 0);
+      mma_frag(acc, y);
+#ifndef BGP_EXP_NO_BAR
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gs.empty[cur]);
+#endif
+    }
+    BGP_LOAD(y, 1);
+    mma_frag(acc, x);
+    BGP_LOAD(x, 2);
+    mma_frag(acc, y);
+    BGP_LOAD(y, 3);
+    mma_frag(acc, x);
+    mma_frag(acc, y);
+#undef BGP_LOAD
+#ifndef BGP_EXP_NO_BAR
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&gs.empty[stage]);
+#endif
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
     }
 
     // ------------------------------- epilogue -------------------------------
-    // Per warp (no group barrier): stage the warp's 64x32 result in its own
-    // 16 KB slice and issue four 16x32 TMA boxes.  beta = 1 (updates): stage
-    // -acc and TMA reduce-add it into C in L2 -- no C load, no read-modify-
-    // write on the critical path.  beta = 0 (V^T V, L X): TMA store of acc.
-    if (store_pending && lane == 0) tma_store_wait_read0();  // slice free again
-    __syncwarp();
-    uint8_t* cw = gs.cbuf + gwarp * WSTAGE_BYTES;
+    // Per warp (no group barrier), in two rounds of 32 rows: stage the rows in
+    // the warp's own 8 KB slice and issue two 16x32 TMA boxes.  beta = 1
+    // (updates): stage -acc and TMA reduce-add it into C in L2 -- no C load,
+    // no read-modify-write on the critical path.  beta = 0 (V^T V, L X): TMA
+    // store of acc.  A round waits only until the previous round's boxes
+    // were read out of shared memory.
+#ifdef BGP_EXP_NO_EPI  // probe build: no epilogue
+    {
+      double sum = 0.0;
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int m = it.mrow0 + wm * WM + i * 8 + q;
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
-          double* ptr = reinterpret_cast<double*>(cw + lane_off(i & 1, e, q, s4) + (i >> 1) * WBOX_BYTES +
-                                                  j * 8 * 128);
-          const bool keep = it.lower && m < n;  // strict upper triangle stays
-          *ptr = keep ? 0.0 : (accumulate ? -acc[i][j][e] : acc[i][j][e]);
-        }
-      }
+        for (int j = 0; j < NJ; ++j) sum += acc[i][j][0] + acc[i][j][1];
+      if (sum == 12345.678) gs.cbuf[0] = 1;
     }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      const int r0 = it.mrow0 + wm * WM, c0 = it.nrow0 + wn * WN;
+    continue;
+#endif
+#ifdef BGP_EXP_TRACE
+    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+      g_trace[blockIdx.x][g][t_idx][1] = clock64();
+#endif
 #pragma unroll
-      for (int i = 0; i < WM / 16; ++i) {
-        if (accumulate)
-          tma_reduce_add_3d(tmC, cw + i * WBOX_BYTES, r0 + i * 16, c0, (int)it.cTile, pol_stream);
-        else
-          tma_store_3d(tmC, cw + i * WBOX_BYTES, r0 + i * 16, c0, (int)it.cTile, pol_stream);
+    for (int r = 0; r < 2; ++r) {
+      if (lane == 0 && (store_pending || r == 1)) tma_store_wait_read0();  // slice free again
+      __syncwarp();
+      // row m = m0 + ii*8 of the round, column n = n0 + j*8 + e (tile coordinates)
+      const int m0 = it.mrow0 + wm * WM + r * (WM / 2) + q, n0 = it.nrow0 + wn * WN + 2 * s4;
+      if (it.lower) {
+        if (r == 0) stage_rows<0, ACC, true>(acc, cbase, m0, n0);
+        else stage_rows<1, ACC, true>(acc, cbase, m0, n0);
+      } else {
+        if (r == 0) stage_rows<0, ACC, false>(acc, cbase, m0, n0);
+        else stage_rows<1, ACC, false>(acc, cbase, m0, n0);
       }
-      tma_store_commit();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int r0 = it.mrow0 + wm * WM + r * (WM / 2), c0 = it.nrow0 + wn * WN;
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+          if (ACC)
+            tma_reduce_add_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+          else
+            tma_store_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+        }
+        tma_store_commit();
+      }
     }
     store_pending = true;
+#ifdef BGP_EXP_TRACE
+    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+      g_trace[blockIdx.x][g][t_idx][2] = clock64();
+#endif
+  }
+  if (stagger_arrive) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(stagger);
   }
   if (lane == 0 && store_pending) tma_store_wait_all0();
 }
@@ -340,15 +512,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(&gs.full[s], 1);
         mbar_init(&gs.empty[s], GROUP_WARPS);
       }
-      mbar_init(gs.c_full, 1);
-      mbar_init(gs.c_empty, 1);
     }
+    mbar_init(stagger_bar(smem), GROUP_WARPS);
     fence_barrier_init();
   }
   __syncthreads();
 
   const int64_t nitems = gemm_num_items(p);
-  const bool accumulate = (p.beta != 0.0);  // (alpha, beta) = (-1, 1) or (1, 0)
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (warp < GROUPS && lane == 0)
@@ -356,7 +526,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     const int g = wg - 1;
-    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, accumulate);
+    // (alpha, beta) = (-1, 1): C -= A B^T by reduce-add;  (1, 0): C = A B^T
+    if (p.beta != 0.0)
+      consumer_loop<true>(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, stagger_bar(smem));
+    else
+      consumer_loop<false>(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, stagger_bar(smem));
   }
 }
 
@@ -407,3 +581,9 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
 }
 
 }  // namespace bgp
+
+#ifdef BGP_EXP_TRACE
+extern "C" int bgp_probe_trace(void* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, bgp::g_trace, sizeof(bgp::g_trace));
+}
+#endif

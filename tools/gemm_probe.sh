@@ -1,0 +1,24 @@
+#!/bin/bash
+# Build probe variants of libbgp (experiment macros in gemm.cu) and time them.
+# Usage: bash tools/gemm_probe.sh build   (here)   |   bash tools/gemm_probe.sh run (GPU box)
+set -e
+D=build/probe
+if [ "$1" = "build" ]; then
+  mkdir -p $D
+  for v in ${VARIANTS:-base NO_TMA NO_EPI NO_TMA_NO_EPI NO_BAR}; do
+    case $v in
+      base) F="";; NO_TMA) F="-DBGP_EXP_NO_TMA";; NO_EPI) F="-DBGP_EXP_NO_EPI";;
+      NO_TMA_NO_EPI) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
+      TRACE) F="-DBGP_EXP_TRACE";;
+      NO_BAR) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR";;
+    esac
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $F $EXTRA \
+      -c paper_1305_4886_b200/csrc/gemm.cu -o $D/gemm_$v.o
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/libbgp_$v.so build/capi.o build/cov.o \
+      build/potrf.o $D/gemm_$v.o build/solve.o build/rng.o
+  done
+else
+  mkdir -p gpurun_out/probe
+  L=""; for v in ${VARIANTS:-base NO_TMA NO_EPI NO_TMA_NO_EPI NO_BAR}; do L="$L $D/libbgp_$v.so"; done
+  python tools/gemm_probe.py $L 2>&1 | tee gpurun_out/probe/gemm_probe.log
+fi
