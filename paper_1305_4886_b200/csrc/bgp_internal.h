@@ -35,6 +35,8 @@ struct Ctx {
   size_t part_cap = 0;
   int32_t* d_items = nullptr;
   size_t items_cap = 0;
+  int* d_sync = nullptr;  // persistent-kernel row counter + ready flags
+  size_t sync_cap = 0;
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)
   bool profile = false;
@@ -87,6 +89,7 @@ struct GemmProblem {
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s);
 
+int launch_trsv_fwd_persistent(Ctx* ctx, const double* L, int64_t n, int b, double* x, cudaStream_t s);
 int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s);
 int launch_trsm_rect_back(Ctx* ctx, const double* L, int64_t n, int b, double* Bt, int64_t m,
                           cudaStream_t s);

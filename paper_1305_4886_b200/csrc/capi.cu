@@ -160,6 +160,7 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_dinv) cudaFree(ctx->d_dinv);
   if (ctx->d_part) cudaFree(ctx->d_part);
   if (ctx->d_items) cudaFree(ctx->d_items);
+  if (ctx->d_sync) cudaFree(ctx->d_sync);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
   delete[] ctx->events;
   delete ctx;

@@ -153,15 +153,7 @@ __global__ void __launch_bounds__(256) trsv_update_back_kernel(const double* __r
 int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s) {
   const int T = (int)((n + b - 1) / b);
   if (!trans) {
-    for (int J = 0; J < T; ++J) {
-      trsv_diag_fwd_kernel<<<1, 256, 0, s>>>(L + tri_index(J, J, T) * (int64_t)b * b, b, n, (int64_t)J * b,
-                                             x + (int64_t)J * b, ctx->d_info);
-      ctx->launches++;
-      if (J + 1 < T) {
-        trsv_update_fwd_kernel<<<T - J - 1, 256, 0, s>>>(L, T, b, J, x, ctx->d_info);
-        ctx->launches++;
-      }
-    }
+    return launch_trsv_fwd_persistent(ctx, L, n, b, x, s);
   } else {
     for (int J = T - 1; J >= 0; --J) {
       trsv_diag_back_kernel<<<1, 256, 0, s>>>(L + tri_index(J, J, T) * (int64_t)b * b, b, n, (int64_t)J * b,
