@@ -217,15 +217,19 @@ int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
                     int64_t count, int tile, void* stream);
 
 /* ---- measurement ----------------------------------------------------------
- * When profiling is on, bgp_potrf brackets every launch with CUDA events on
- * the caller's stream (no extra synchronization: they are read at the
- * status sync the call already does).  bgp_profile_read returns and clears
- *   out[0] potrf ms  out[1] trsm ms  out[2] gemm (trailing update) ms
- *   out[3] gemm launches  out[4] gemm algorithmic flops (b^3 k^2 per launch)
+ * When profiling is on, bgp_potrf brackets every launch with CUDA events
+ * (no extra synchronization: they are read at the status sync the call
+ * already does).  bgp_profile_read returns and clears BGP_PROFILE_SLOTS values:
+ *   out[0] potrf ms (look-ahead stream, overlaps the trailing update)
+ *   out[1] trsm ms  out[2] gemm (trailing update, both parts) ms
+ *   out[3] gemm launches  out[4] gemm algorithmic flops (b^3 k^2 per step)
  *   out[5] potrf launches  out[6] trsm launches  out[7] factorizations
+ *   out[8] factorization ms (first to last launch on the caller's stream)
+ *   out[9] potrf ms exposed on the critical path (caller's stream waiting)
  * (stands in for the reference's event log, bg/transport/base.py:121-123). */
+#define BGP_PROFILE_SLOTS 10
 int bgp_set_profiling(bgp_ctx_t ctx, int on);
-int bgp_profile_read(bgp_ctx_t ctx, double* out8);
+int bgp_profile_read(bgp_ctx_t ctx, double* out);
 
 #ifdef __cplusplus
 }

@@ -37,12 +37,18 @@ struct Ctx {
   size_t items_cap = 0;
   int* d_sync = nullptr;  // persistent-kernel row counter + ready flags
   size_t sync_cap = 0;
+  int* d_gate = nullptr;  // per-step look-ahead counters of the Cholesky
+  size_t gate_cap = 0;
+  double* d_linv = nullptr;  // inverse of the current diagonal tile (panel TRSM on DMMA)
+  size_t linv_cap = 0;
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)
   bool profile = false;
   cudaEvent_t* events = nullptr;
   int events_cap = 0;
-  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double prof[BGP_PROFILE_SLOTS] = {};
+  cudaStream_t side = nullptr;  // look-ahead stream (tile POTRF of the next panel)
+  cudaEvent_t ev_col = nullptr, ev_fact = nullptr;
 };
 
 int set_err(Ctx* ctx, const char* what, cudaError_t e);
@@ -66,14 +72,31 @@ int launch_tile_gemv(Ctx* ctx, const double* base, const int32_t* items, int64_t
 int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_t count, int b, int64_t n,
                        cudaStream_t s);
 
+// one-time kernel attribute setup; also loads the modules eagerly (lazy
+// loading must not happen while a look-ahead kernel spin-waits)
+void gemm_prepare();
+void potrf_prepare();
+
 // tile kernels
-int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s);
+// info value reserved for a look-ahead wait that never completed (a bug, not data)
+constexpr unsigned long long BGP_INFO_DATAFLOW_TIMEOUT = 1ull << 62;
+int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
+                      const int* gate = nullptr, int gate_need = 0);
+int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
                       int trans, cudaStream_t s, bool check_info = true);
 
 // DMMA/TMA GEMM problems
-enum GemmMode { GEMM_CHOL_TRAIL = 0, GEMM_RECT_TRAIL = 1, GEMM_SYRK_RECT = 2, GEMM_LIST = 3, GEMM_TRMM_RECT = 4 };
+enum GemmMode {
+  GEMM_CHOL_TRAIL = 0,  // tiles (R, C), J+1+coff <= C <= R < T, of the step-J trailing update
+  GEMM_RECT_TRAIL = 1,
+  GEMM_SYRK_RECT = 2,
+  GEMM_LIST = 3,
+  GEMM_TRMM_RECT = 4,
+  GEMM_CHOL_COL = 5,    // tiles (R, J+1), J+1 <= R < T: the next panel's column (look-ahead)
+  GEMM_TRSM_PANEL = 6   // X = A Linv^T in place for `count` consecutive tiles from panel0
+};
 struct GemmProblem {
   int mode;
   int b;
@@ -85,6 +108,11 @@ struct GemmProblem {
   const int32_t* items;
   double alpha, beta;  // D = beta*C + alpha*sum(A B^T)
   bool check_info;     // skip the launch when ctx->d_info records a failure
+  int coff;            // GEMM_CHOL_TRAIL: skip the first coff trailing columns
+  int* signal;         // != null: +1 per warp when its part of tile signal_tile is in L2
+  int64_t signal_tile;
+  int64_t panel0;      // GEMM_TRSM_PANEL: tile index of the first panel tile
+  int grid_limit;      // > 0: at most this many CTAs (leaves SMs to a concurrent kernel)
 };
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s);

@@ -8,6 +8,7 @@
 // the only host synchronization is the final status read.
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cmath>
@@ -142,6 +143,11 @@ int bgp_init(int device, bgp_ctx_t* out) {
     e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ctx->encode_fn, cudaEnableDefault, &q);
     if (e == cudaSuccess && q != cudaDriverEntryPointSuccess) e = cudaErrorNotSupported;
   }
+  if (e == cudaSuccess) {
+    gemm_prepare();
+    potrf_prepare();
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) {
     fprintf(stderr, "bgp_init: %s\n", cudaGetErrorString(e));
     delete ctx;
@@ -161,6 +167,11 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_part) cudaFree(ctx->d_part);
   if (ctx->d_items) cudaFree(ctx->d_items);
   if (ctx->d_sync) cudaFree(ctx->d_sync);
+  if (ctx->d_gate) cudaFree(ctx->d_gate);
+  if (ctx->d_linv) cudaFree(ctx->d_linv);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
+  if (ctx->ev_fact) cudaEventDestroy(ctx->ev_fact);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
   delete[] ctx->events;
   delete ctx;
@@ -180,6 +191,26 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen, const doubl
   return construct(ctx, kind, g, X, nx, Y, ny, tile, out, (cudaStream_t)stream);
 }
 
+// number of 128x64 GEMM blocks of a diagonal tile (the rest lie strictly
+// above the diagonal and are skipped); gemm.cu diag_block
+static int diag_tile_blocks(int b) {
+  int c = 0;
+  for (int bi = 0; bi < b / 128; ++bi)
+    for (int bj = 0; bj < b / 64; ++bj) c += (bi * 128 + 127 >= bj * 64);
+  return c;
+}
+
+// Right-looking tile Cholesky with a one-panel look-ahead.  The step-J
+// trailing update is one persistent DMMA launch on all SMs but one; its
+// first blocks (static order) are those of tile column J+1, and the warps
+// that reduce into the diagonal tile (J+1, J+1) bump a per-step counter once
+// their bulk reductions retired.  The tile POTRF of J+1 is launched on the
+// side stream at the same time: it waits on that counter and factors the
+// tile on the spare SM while the rest of the update runs, so the
+// latency-bound one-CTA factorization leaves the critical path.  The panel
+// TRSM of J+1 then waits for both.  Nothing waits on the POTRF except through
+// stream events, so the dependency is one-way and cannot deadlock.  The only
+// host synchronization is the final status read.
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
   if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -189,10 +220,55 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   if (rc) return rc;
   const size_t dinv_bytes = (size_t)(b / 32) * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * sizeof(int)))) return rc;
+  if (!ctx->side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_col, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fact, cudaEventDisableTiming);
+    if (e != cudaSuccess) return set_err(ctx, "look-ahead stream", e);
+  }
+  {
+    cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * sizeof(int), s);
+    if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
+  }
   const int64_t ntiles = tri_count(T);
   const int64_t tsz = (int64_t)b * b;
-  // profiling: event k brackets launch k (potrf, trsm, gemm per panel)
-  const int nev = 3 * T + 1;
+  const int gate_need = diag_tile_blocks(b) * 4;  // 4 warps per block (gemm.cu GROUP_WARPS)
+  gemm_prepare();
+  potrf_prepare();
+  if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
+  // BGP_TRSM (diagnostics): 1 (default) panel TRSM on the DMMA GEMM with the
+  // tile inverse; 0 the FP64 substitution kernel
+  static const int trsm_mode = [] {
+    const char* e = getenv("BGP_TRSM");
+    return e ? atoi(e) : 1;
+  }();
+  // after POTRF(K) on stream st: what the panel solve of K needs
+  auto after_potrf = [&](int K, cudaStream_t st) -> int {
+    if (trsm_mode == 0 || K + 1 >= T) return BGP_OK;
+    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st);
+  };
+  // panel solve of K on the caller's stream: L_IK = A_IK L_KK^{-T}, I > K
+  auto panel_solve = [&](int K) -> int {
+    if (K + 1 >= T) return BGP_OK;
+    double* panel = tiles + tri_index(K + 1, K, T) * tsz;
+    if (trsm_mode == 0)
+      return launch_panel_trsm(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, panel, T - K - 1, b, 0, s);
+    GemmProblem p{};
+    p.mode = GEMM_TRSM_PANEL;
+    p.b = b;
+    p.T = T;
+    p.J = K;
+    p.count = T - K - 1;
+    p.panel0 = tri_index(K + 1, K, T);
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    p.check_info = true;
+    return launch_gemm(ctx, p, tiles, tiles, ntiles, ctx->d_linv, 1, ntiles, s);
+  };
+  // profiling: main-stream marks (start, potrf0, trsm0, then gemm / wait / trsm
+  // per step) and side-stream potrf start/end pairs
+  const int nev = 5 * T + 4;
   if (ctx->profile && ctx->events_cap < nev) {
     for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
     delete[] ctx->events;
@@ -201,18 +277,38 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     ctx->events_cap = nev;
   }
   int ev = 0;
-  auto mark = [&]() {
-    if (ctx->profile) cudaEventRecord(ctx->events[ev++], s);
+  auto mark = [&](cudaStream_t st) -> int {
+    if (!ctx->profile || ev >= ctx->events_cap) return -1;
+    cudaEventRecord(ctx->events[ev], st);
+    return ev++;
   };
-  mark();
-  for (int J = 0; J < T; ++J) {
-    double* djj = tiles + tri_index(J, J, T) * tsz;
-    if ((rc = launch_tile_potrf(ctx, djj, b, (int64_t)J * b, ctx->d_dinv, s))) return rc;
-    mark();
-    if (J + 1 < T) {
-      double* panel = tiles + tri_index(J + 1, J, T) * tsz;
-      if ((rc = launch_panel_trsm(ctx, djj, ctx->d_dinv, panel, T - J - 1, b, 0, s))) return rc;
-      mark();
+  auto el = [&](int a, int c) -> double {
+    float ms = 0.f;
+    if (a >= 0 && c >= 0) cudaEventElapsedTime(&ms, ctx->events[a], ctx->events[c]);
+    return (double)ms;
+  };
+  struct StepMarks {
+    int gemm_end, wait_end, trsm_end, p0, p1;
+  };
+  static thread_local StepMarks sm_[4096];
+  const int m_start = mark(s);
+  if ((rc = launch_tile_potrf(ctx, tiles, b, 0, ctx->d_dinv, s))) return rc;
+  if ((rc = after_potrf(0, s))) return rc;
+  const int m_p0 = mark(s);
+  if ((rc = panel_solve(0))) return rc;
+  int m_prev = mark(s);
+  const int m_t0 = m_prev;
+  // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead; 0 sequential on
+  // all SMs; 2 sequential with the trailing update on all SMs but one
+  static const int la_mode = [] {
+    const char* e = getenv("BGP_LOOKAHEAD");
+    return e ? atoi(e) : 1;
+  }();
+  for (int J = 0; J + 1 < T; ++J) {
+    const int K = J + 1;  // next panel
+    double* dkk = tiles + tri_index(K, K, T) * tsz;
+    StepMarks sm{-1, -1, -1, -1, -1};
+    if (la_mode != 1) {
       GemmProblem p{};
       p.mode = GEMM_CHOL_TRAIL;
       p.b = b;
@@ -221,33 +317,74 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
       p.alpha = -1.0;
       p.beta = 1.0;
       p.check_info = true;
+      p.grid_limit = la_mode == 2 ? ctx->num_sms - 1 : 0;
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
-      mark();
+      sm.gemm_end = mark(s);
+      sm.p0 = mark(s);
+      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, s))) return rc;
+      if ((rc = after_potrf(K, s))) return rc;
+      sm.p1 = sm.wait_end = mark(s);
+      if ((rc = panel_solve(K))) return rc;
+      sm.trsm_end = mark(s);
+      if (J < 4096) sm_[J] = sm;
+      continue;
     }
+    // POTRF(K) may start once TRSM(J) released the shared inverse buffer
+    cudaEventRecord(ctx->ev_col, s);
+    cudaStreamWaitEvent(ctx->side, ctx->ev_col, 0);
+    sm.p0 = mark(ctx->side);
+    if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, ctx->side, ctx->d_gate + J,
+                                gate_need)))
+      return rc;
+    if ((rc = after_potrf(K, ctx->side))) return rc;
+    sm.p1 = mark(ctx->side);
+    cudaEventRecord(ctx->ev_fact, ctx->side);
+    GemmProblem p{};
+    p.mode = GEMM_CHOL_TRAIL;
+    p.b = b;
+    p.T = T;
+    p.J = J;
+    p.alpha = -1.0;
+    p.beta = 1.0;
+    p.check_info = true;
+    p.grid_limit = ctx->num_sms - 1;  // the spare SM runs POTRF(K)
+    p.signal = ctx->d_gate + J;
+    p.signal_tile = tri_index(K, K, T);
+    if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
+    sm.gemm_end = mark(s);
+    cudaStreamWaitEvent(s, ctx->ev_fact, 0);
+    sm.wait_end = mark(s);
+    if ((rc = panel_solve(K))) return rc;
+    sm.trsm_end = mark(s);
+    if (J < 4096) sm_[J] = sm;
   }
   rc = read_info(ctx, s, info);
+  if (rc == BGP_OK && info && (unsigned long long)*info >= BGP_INFO_DATAFLOW_TIMEOUT) {
+    ctx->err = "look-ahead POTRF wait timed out (internal dependency error)";
+    return BGP_E_CUDA;
+  }
   if (rc == BGP_OK && ctx->profile) {
-    // events: [0] start, then per panel potrf | trsm | gemm boundaries
-    int k = 0;
-    for (int J = 0; J < T; ++J) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
-      ctx->prof[0] += ms;
+    ctx->prof[0] += el(m_start, m_p0);  // potrf(0): on the critical path
+    ctx->prof[9] += el(m_start, m_p0);
+    ctx->prof[5] += 1;
+    ctx->prof[1] += el(m_p0, m_t0);
+    ctx->prof[6] += 1;
+    int last = m_t0;
+    for (int J = 0; J + 1 < T && J < 4096; ++J) {
+      const StepMarks& m = sm_[J];
+      ctx->prof[2] += el(m_prev, m.gemm_end);
+      ctx->prof[3] += 1;
+      ctx->prof[9] += el(m.gemm_end, m.wait_end);
+      ctx->prof[1] += el(m.wait_end, m.trsm_end);
+      ctx->prof[6] += 1;
+      ctx->prof[0] += el(m.p0, m.p1);
       ctx->prof[5] += 1;
-      ++k;
-      if (J + 1 < T) {
-        cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
-        ctx->prof[1] += ms;
-        ctx->prof[6] += 1;
-        ++k;
-        cudaEventElapsedTime(&ms, ctx->events[k], ctx->events[k + 1]);
-        ctx->prof[2] += ms;
-        ctx->prof[3] += 1;
-        const double kk = (double)(T - J - 1);
-        ctx->prof[4] += (double)b * b * b * kk * kk;
-        ++k;
-      }
+      const double kk = (double)(T - J - 1);
+      ctx->prof[4] += (double)b * b * b * kk * kk;
+      m_prev = m.trsm_end;
+      last = m.trsm_end;
     }
+    ctx->prof[8] += el(m_start, last);
     ctx->prof[7] += 1;
   }
   return rc;
@@ -258,9 +395,9 @@ int bgp_set_profiling(bgp_ctx_t ctx, int on) {
   return BGP_OK;
 }
 
-int bgp_profile_read(bgp_ctx_t ctx, double* out8) {
-  for (int i = 0; i < 8; ++i) {
-    out8[i] = ctx->prof[i];
+int bgp_profile_read(bgp_ctx_t ctx, double* out) {
+  for (int i = 0; i < BGP_PROFILE_SLOTS; ++i) {
+    out[i] = ctx->prof[i];
     ctx->prof[i] = 0.0;
   }
   return BGP_OK;

@@ -69,25 +69,35 @@ struct Item {
   int nkt;                   // number of k tiles
   int mrow0, nrow0;          // row offsets inside the A / B tiles (= C block offsets)
   int lower;                 // block straddles the diagonal of a diagonal tile
+  int kstages;               // > 0: number of BK stages (triangular k range), else nkt * b / BK
   bool valid;
 };
 
-__device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
+__host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
   const int nblk = (p.b / BM) * (p.b / BN);
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
-      const int64_t k = p.T - p.J - 1;
-      return k * (k + 1) / 2 * nblk;
+      const int64_t k = p.T - p.J - 1 - p.coff;
+      return k > 0 ? k * (k + 1) / 2 * nblk : 0;
     }
+    case GEMM_CHOL_COL:
+      return (int64_t)(p.T - p.J - 1) * nblk;
     case GEMM_RECT_TRAIL:
       return (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
     case GEMM_SYRK_RECT:
       return (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
     case GEMM_TRMM_RECT:
       return (int64_t)p.Tm * p.T * nblk;
-    default:
+    default:  // GEMM_LIST, GEMM_TRSM_PANEL
       return p.count * nblk;
   }
+}
+
+// blocks of one task that the same consumer group must run back to back
+// (TRSM: the column blocks of a 128-row slab, right to left, so the in-place
+// solve never overwrites columns a later block still reads)
+__host__ __device__ __forceinline__ int gemm_passes(const GemmProblem& p) {
+  return p.mode == GEMM_TRSM_PANEL ? p.b / BN : 1;
 }
 
 // diagonal-tile block (bi, bj): skip blocks strictly above the diagonal,
@@ -111,11 +121,32 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
   it.valid = true;
   it.lower = 0;
   it.bTriRow = -1;
+  it.kstages = 0;
   switch (p.mode) {
+    case GEMM_TRSM_PANEL: {  // item = task * nbn + pass, task = tile * (b/BM) + row block
+      const int pass = (int)(item % nbn);
+      const int64_t task = item / nbn;
+      const int nbm = p.b / BM;
+      const int bjj = nbn - 1 - pass;
+      it.mrow0 = (int)(task % nbm) * BM;
+      it.nrow0 = bjj * BN;
+      it.cTile = it.aTile0 = p.panel0 + task / nbm;
+      it.bTile0 = 0;                     // Linv (single tile)
+      it.kstages = (bjj + 1) * BN / BK;  // Linv(n, k) = 0 for k > n
+      break;
+    }
     case GEMM_CHOL_TRAIL: {
       int rr, cc;
-      tri_decode(t, p.T - p.J - 1, rr, cc);
-      const int R = p.J + 1 + rr, C = p.J + 1 + cc;
+      tri_decode(t, p.T - p.J - 1 - p.coff, rr, cc);
+      const int R = p.J + 1 + p.coff + rr, C = p.J + 1 + p.coff + cc;
+      it.cTile = tri_index(R, C, p.T);
+      it.aTile0 = tri_index(R, p.J, p.T);
+      it.bTile0 = tri_index(C, p.J, p.T);
+      if (R == C) diag_block(it, bi, bj);
+      break;
+    }
+    case GEMM_CHOL_COL: {
+      const int R = p.J + 1 + (int)t, C = p.J + 1;
       it.cTile = tri_index(R, C, p.T);
       it.aTile0 = tri_index(R, p.J, p.T);
       it.bTile0 = tri_index(C, p.J, p.T);
@@ -209,11 +240,13 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const 
   const int kc_per_tile = p.b / BK;
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
-       item += (int64_t)GROUPS * gridDim.x) {
-    const Item it = gemm_decode(p, item);
+  const int npass = gemm_passes(p);
+  for (int64_t task = blockIdx.x + (int64_t)g * gridDim.x; task * npass < nitems;
+       task += (int64_t)GROUPS * gridDim.x)
+  for (int pass = 0; pass < npass; ++pass) {
+    const Item it = gemm_decode(p, task * npass + pass);
     if (!it.valid) continue;
-    const int nk = it.nkt * kc_per_tile;
+    const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
     for (int kc = 0; kc < nk; ++kc) {
       mbar_wait(&gs.empty[stage], phase ^ 1);
 #ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
@@ -359,11 +392,14 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   bool stagger_arrive = (g == 0);
   if (g == 1) mbar_wait(stagger, 0);
 
-  for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < nitems;
-       item += (int64_t)GROUPS * gridDim.x) {
+  const int npass = gemm_passes(p);
+  for (int64_t task = blockIdx.x + (int64_t)g * gridDim.x; task * npass < nitems;
+       task += (int64_t)GROUPS * gridDim.x)
+  for (int pass = 0; pass < npass; ++pass) {
+    const int64_t item = task * npass + pass;
     const Item it = gemm_decode(p, item);
     if (!it.valid) continue;
-    const int nk = it.nkt * kc_per_tile;
+    const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -483,6 +519,17 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       }
     }
     store_pending = true;
+    if (p.signal && it.cTile == p.signal_tile) {
+      // look-ahead: the next panel's diagonal tile is complete once every warp
+      // that reduces into it has its bulk ops retired
+      if (lane == 0) {
+        tma_store_wait_all0();
+        fence_proxy_async_global();
+        __threadfence();
+        atomicAdd(p.signal, 1);
+      }
+      __syncwarp();
+    }
 #ifdef BGP_EXP_TRACE
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][2] = clock64();
@@ -534,37 +581,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
-                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s) {
-  if (p.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
-  int64_t items;
-  {
-    const int64_t nblk = (int64_t)(p.b / BM) * (p.b / BN);
-    switch (p.mode) {
-      case GEMM_CHOL_TRAIL: {
-        const int64_t k = p.T - p.J - 1;
-        items = k * (k + 1) / 2 * nblk;
-        break;
-      }
-      case GEMM_RECT_TRAIL:
-        items = (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
-        break;
-      case GEMM_SYRK_RECT:
-        items = (int64_t)p.Tm * (p.Tm + 1) / 2 * nblk;
-        break;
-      case GEMM_TRMM_RECT:
-        items = (int64_t)p.Tm * p.T * nblk;
-        break;
-      default:
-        items = p.count * nblk;
-    }
-  }
-  if (items <= 0) return BGP_OK;
-  CUtensorMap mA, mB, mC;
-  int rc;
-  if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
-  if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
-  if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
+// One-time function setup.  It also forces the module to load: with CUDA's
+// lazy loading, the first launch of a kernel while a spin-waiting kernel runs
+// on another stream (the look-ahead POTRF) could otherwise stall behind it.
+void gemm_prepare() {
   static int occupancy = -1;
   if (occupancy < 0) {
     cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -572,8 +592,22 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, gemm_dmma_kernel, THREADS, SMEM_BYTES);
     if (occupancy < 1) fprintf(stderr, "libbgp: gemm_dmma_kernel cannot be resident\n");
   }
-  const int64_t slots = ctx->num_sms;
-  const int64_t grid = items < slots ? items : slots;
+}
+
+int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
+                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s) {
+  if (p.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
+  const int64_t items = gemm_num_items(p);
+  if (items <= 0) return BGP_OK;
+  CUtensorMap mA, mB, mC;
+  int rc;
+  if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
+  if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
+  if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
+  gemm_prepare();
+  const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
+  const int64_t tasks = items / gemm_passes(p);
+  const int64_t grid = tasks < slots ? tasks : slots;
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mC, p,
                                                                   p.check_info ? ctx->d_info : nullptr);
   ctx->launches++;

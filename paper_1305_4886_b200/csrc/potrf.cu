@@ -146,7 +146,7 @@ __device__ __forceinline__ void tile_trailing(double* A, int b, int base_rc, con
 // diagonal block k+1, so the serial 32x32 work overlaps the DMMA update.
 __global__ void __launch_bounds__(POTRF_THREADS, 1)
     tile_potrf_kernel(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
-                      unsigned long long* __restrict__ info) {
+                      unsigned long long* __restrict__ info, const int* __restrict__ gate, int gate_need) {
   extern __shared__ double sm[];
   double* D = sm;                // 32 x 33
   double* Dinv_s = D + NB * 33;  // 32 x 33
@@ -156,8 +156,30 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (info && *(volatile unsigned long long*)info != 0ull) return;  // an earlier step failed
-  if (tid == 0) s_fail = 0;
+  if (tid == 0) {
+    s_fail = 0;
+    // look-ahead gate: the concurrently running trailing update signals when
+    // every block of this tile has been reduced into L2 (release/acquire)
+    if (gate) {
+      unsigned ns = 64;
+      long long spins = 0;
+      while (ld_acquire_gpu(gate) < gate_need) {
+        if (*(volatile unsigned long long*)info != 0ull) {
+          s_fail = 1;
+          break;
+        }
+        if (++spins > (1ll << 24)) {  // ~minutes: a broken dependency, not a slow GPU
+          set_info(info, (long long)BGP_INFO_DATAFLOW_TIMEOUT);
+          s_fail = 1;
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 2048) ns <<= 1;
+      }
+    }
+  }
   __syncthreads();
+  if (s_fail) return;
   const int nbk = b / NB;
   // prologue: factor + invert diagonal block 0
   if (warp == 0) {
@@ -220,6 +242,58 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
     }
     __syncthreads();
     if (s_fail) return;
+  }
+}
+
+// Full inverse of a factored diagonal tile, Linv = L^{-1} (column-major b x b,
+// zero strict upper triangle), from its 32x32 diagonal-block inverses:
+//   Linv[i][j] = -Dinv_i * sum_{m=j}^{i-1} L[i][m] Linv[m][j]     (i > j)
+// One CTA per 32-wide column block j; it keeps its column of Linv blocks in
+// shared memory.  Feeds the panel TRSM on the DMMA GEMM (X = A Linv^T).
+__global__ void __launch_bounds__(256) tri_inv_kernel(const double* __restrict__ L,
+                                                      const double* __restrict__ dinv, int b,
+                                                      double* __restrict__ Linv) {
+  extern __shared__ double xs[];  // Linv blocks (i, j), i >= j: [(i-j)*32 + r]*33 + c
+  double* tmp = xs + (size_t)(b / NB) * NB * 33;  // 32 x 33
+  const int j = blockIdx.x, nbk = b / NB;
+  const int tid = threadIdx.x, r = tid & 31, c8 = tid >> 5;
+  for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
+    const int c = idx >> 5, rr = idx & 31;
+    xs[rr * 33 + c] = dinv[(int64_t)j * NB * NB + idx];
+  }
+  __syncthreads();
+  for (int i = j + 1; i < nbk; ++i) {
+    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int m = j; m < i; ++m) {
+      const double* Xm = xs + (size_t)(m - j) * NB * 33;
+#pragma unroll 8
+      for (int q = 0; q < NB; ++q) {
+        const double l = L[(int64_t)(m * NB + q) * b + i * NB + r];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sacc[u] = fma(l, Xm[q * 33 + c8 + 8 * u], sacc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tmp[r * 33 + c8 + 8 * u] = sacc[u];
+    __syncthreads();
+    const double* Di = dinv + (int64_t)i * NB * NB;  // column-major: (r, q) at q*32 + r
+    double* Xi = xs + (size_t)(i - j) * NB * 33;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c8 + 8 * u;
+      double v = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < NB; ++q) v = fma(Di[q * NB + r], tmp[q * 33 + c], v);
+      Xi[r * 33 + c] = -v;
+    }
+    __syncthreads();
+  }
+  // column block j of Linv: rows < 32j are zero
+  for (int idx = tid; idx < NB * b; idx += blockDim.x) {
+    const int c = idx / b, row = idx % b;
+    const int blk = row / NB;
+    const double v = (blk < j) ? 0.0 : xs[((size_t)(blk - j) * NB + (row & 31)) * 33 + c];
+    Linv[(int64_t)(j * NB + c) * b + row] = v;
   }
 }
 
@@ -329,16 +403,32 @@ __global__ void __launch_bounds__(TRSM_THREADS, 2)
   }
 }
 
-int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s) {
-  const size_t smem = (size_t)(2 * NB * 33 + (b - NB) * PLD) * sizeof(double);
-  static bool attr_done = false;
-  if (!attr_done) {
+void potrf_prepare() {
+  static bool done = false;
+  if (!done) {
     cudaFuncSetAttribute(tile_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
+    cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, diag_inv_kernel);
+    done = true;
   }
-  tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info);
+}
+
+int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
+                      const int* gate, int gate_need) {
+  const size_t smem = (size_t)(2 * NB * 33 + (b - NB) * PLD) * sizeof(double);
+  potrf_prepare();
+  tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info, gate, gate_need);
   ctx->launches++;
   return check_launch(ctx, "tile_potrf");
+}
+
+int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s) {
+  const size_t smem = ((size_t)(b / NB) * NB * 33 + NB * 33) * sizeof(double);
+  tri_inv_kernel<<<b / NB, 256, smem, s>>>(Ltile, dinv, b, Linv);
+  ctx->launches++;
+  return check_launch(ctx, "tri_inv");
 }
 
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s) {
@@ -352,11 +442,7 @@ int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A,
   if (count <= 0) return BGP_OK;
   (void)trans;
   const size_t smem = ((size_t)b * TRSM_R + TRSM_CH * 33 + NB * 33) * sizeof(double);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
-  }
+  potrf_prepare();
   const int64_t grid = count * (b / TRSM_R);
   panel_trsm_kernel<<<(unsigned)grid, TRSM_THREADS, smem, s>>>(Ld, dinv, A, b,
                                                                       check_info ? ctx->d_info : nullptr);
