@@ -328,7 +328,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tile", type=int, default=256)
+    ap.add_argument("--tile", type=int, default=512)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-samples", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -16,7 +16,7 @@ from paper_1305_4886_b200 import spawn  # noqa: E402
 from paper_1305_4886_b200.gp import KrigeProblem, builtin_spec  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--tile", type=int, default=256)
+ap.add_argument("--tile", type=int, default=512)
 ap.add_argument("--evals", type=int, default=1)
 ap.add_argument("--n", type=int, default=0)
 args = ap.parse_args()
