@@ -299,10 +299,15 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   int m_prev = mark(s);
   const int m_t0 = m_prev;
   // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead; 0 sequential on
-  // all SMs; 2 sequential with the trailing update on all SMs but one
+  // all SMs; 2 sequential with the trailing update on all SMs but one.  The
+  // look-ahead POTRF waits on a kernel running concurrently, so it is off
+  // when kernels are serialised (CUDA_LAUNCH_BLOCKING=1, or Nsight Compute,
+  // which replays kernels one at a time).
   static const int la_mode = [] {
-    const char* e = getenv("BGP_LOOKAHEAD");
-    return e ? atoi(e) : 1;
+    if (const char* e = getenv("BGP_LOOKAHEAD")) return atoi(e);
+    const char* blocking = getenv("CUDA_LAUNCH_BLOCKING");
+    if ((blocking && atoi(blocking) != 0) || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE")) return 0;
+    return 1;
   }();
   for (int J = 0; J + 1 < T; ++J) {
     const int K = J + 1;  // next panel
