@@ -41,6 +41,8 @@ struct Ctx {
   size_t gate_cap = 0;
   double* d_linv = nullptr;  // inverse of the current diagonal tile (panel TRSM on DMMA)
   size_t linv_cap = 0;
+  int* d_queue = nullptr;  // task counter of standalone GEMM launches
+  size_t queue_cap = 0;
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)
   bool profile = false;
@@ -82,19 +84,20 @@ void potrf_prepare();
 constexpr unsigned long long BGP_INFO_DATAFLOW_TIMEOUT = 1ull << 62;
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
                       const int* gate = nullptr, int gate_need = 0);
-int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s);
+// one_cta: the single-CTA block-diagonal variant (look-ahead stream, one free SM)
+int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
+                   int* done = nullptr, bool one_cta = false);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
                       int trans, cudaStream_t s, bool check_info = true);
 
 // DMMA/TMA GEMM problems
 enum GemmMode {
-  GEMM_CHOL_TRAIL = 0,  // tiles (R, C), J+1+coff <= C <= R < T, of the step-J trailing update
+  GEMM_CHOL_TRAIL = 0,  // tiles (R, C), J+1 <= C <= R < T, of the step-J trailing update
   GEMM_RECT_TRAIL = 1,
   GEMM_SYRK_RECT = 2,
   GEMM_LIST = 3,
   GEMM_TRMM_RECT = 4,
-  GEMM_CHOL_COL = 5,    // tiles (R, J+1), J+1 <= R < T: the next panel's column (look-ahead)
   GEMM_TRSM_PANEL = 6   // X = A Linv^T in place for `count` consecutive tiles from panel0
 };
 struct GemmProblem {
@@ -108,14 +111,21 @@ struct GemmProblem {
   const int32_t* items;
   double alpha, beta;  // D = beta*C + alpha*sum(A B^T)
   bool check_info;     // skip the launch when ctx->d_info records a failure
-  int coff;            // GEMM_CHOL_TRAIL: skip the first coff trailing columns
-  int* signal;         // != null: +1 per warp when its part of tile signal_tile is in L2
-  int64_t signal_tile;
-  int64_t panel0;      // GEMM_TRSM_PANEL: tile index of the first panel tile
   int grid_limit;      // > 0: at most this many CTAs (leaves SMs to a concurrent kernel)
+  int64_t panel0;      // GEMM_TRSM_PANEL: tile index of the first panel tile
+  int* queue;          // zeroed task counter (null: launch_gemm provides one)
+  // GEMM_CHOL_TRAIL look-ahead: col_gate[r] counts retired warp-blocks of tile
+  // (J+1+r, J+1); with trsm_next the launch also solves panel J+1 in place,
+  // each tile once col_gate reaches tile_need and *linv_flag reaches linv_need
+  int* col_gate;
+  int trsm_next;
+  int tile_need;
+  const int* linv_flag;
+  int linv_need;
+  int trsm_tail;       // update blocks queued after the fused TRSM tasks (tail filler)
 };
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
-                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s);
+                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv = nullptr);
 
 int launch_trsv_fwd_persistent(Ctx* ctx, const double* L, int64_t n, int b, double* x, cudaStream_t s);
 int launch_trsv(Ctx* ctx, const double* L, int64_t n, int b, double* x, int trans, cudaStream_t s);

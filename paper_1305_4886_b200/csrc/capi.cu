@@ -200,27 +200,34 @@ static int diag_tile_blocks(int b) {
   return c;
 }
 
-// Right-looking tile Cholesky with a one-panel look-ahead.  The step-J
-// trailing update is one persistent DMMA launch on all SMs but one; its
-// first blocks (static order) are those of tile column J+1, and the warps
-// that reduce into the diagonal tile (J+1, J+1) bump a per-step counter once
-// their bulk reductions retired.  The tile POTRF of J+1 is launched on the
-// side stream at the same time: it waits on that counter and factors the
-// tile on the spare SM while the rest of the update runs, so the
-// latency-bound one-CTA factorization leaves the critical path.  The panel
-// TRSM of J+1 then waits for both.  Nothing waits on the POTRF except through
-// stream events, so the dependency is one-way and cannot deadlock.  The only
-// host synchronization is the final status read.
+// Right-looking tile Cholesky with a one-panel look-ahead, two launches per
+// step.  The step-J trailing update is one persistent DMMA launch on all SMs
+// but one.  Its task queue holds the update blocks (tile column J+1 first)
+// followed by the in-place TRSM of panel J+1.  Warps that reduce into a tile
+// of column J+1 bump that tile's counter once their bulk reductions retired.
+// On the side stream, on the spare SM, the tile POTRF of J+1 waits for the
+// diagonal tile's counter, factors it, and tri_inv publishes its inverse;
+// the update's TRSM tasks wait for their tile's counter and that flag.  So the
+// latency-bound POTRF and the panel TRSM both run under the trailing update,
+// and the TRSM fills the update's tail instead of adding a launch.  Waits are
+// one-way (update -> POTRF -> TRSM tasks, never back), bounded, and reported
+// as errors if they ever time out.  The only host synchronization is the
+// final status read.
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
   if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const int b = tile;
   const int T = (int)((n + b - 1) / b);
+  const int nbk = b / 32;
   int rc = reset_info(ctx, s);
   if (rc) return rc;
-  const size_t dinv_bytes = (size_t)(b / 32) * 32 * 32 * sizeof(double);
+  const size_t dinv_bytes = (size_t)nbk * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
-  if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * sizeof(int)))) return rc;
+  // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
+  // published, [stride-2, stride) the 64-bit task counter of the step's launch
+  const int stride = (T + 4 + 1) & ~1;
+  if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
   if (!ctx->side) {
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_col, cudaEventDisableTiming);
@@ -228,47 +235,29 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     if (e != cudaSuccess) return set_err(ctx, "look-ahead stream", e);
   }
   {
-    cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * sizeof(int), s);
+    cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
     if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
   }
-  const int64_t ntiles = tri_count(T);
-  const int64_t tsz = (int64_t)b * b;
-  const int gate_need = diag_tile_blocks(b) * 4;  // 4 warps per block (gemm.cu GROUP_WARPS)
   gemm_prepare();
   potrf_prepare();
-  if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
-  // BGP_TRSM (diagnostics): 1 (default) panel TRSM on the DMMA GEMM with the
-  // tile inverse; 0 the FP64 substitution kernel
-  static const int trsm_mode = [] {
-    const char* e = getenv("BGP_TRSM");
-    return e ? atoi(e) : 1;
+  const int64_t ntiles = tri_count(T);
+  const int64_t tsz = (int64_t)b * b;
+  const int nblk = (b / 128) * (b / 64);                 // 128x64 blocks per tile (gemm.cu)
+  const int diag_need = diag_tile_blocks(b) * 4;         // 4 warps per block (gemm.cu GROUP_WARPS)
+  const int tile_need = nblk * 4;
+  // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead; 0 sequential on
+  // all SMs; 2 sequential with the trailing update on all SMs but one.  The
+  // look-ahead POTRF waits on a kernel running concurrently, so it is off
+  // when kernels are serialised (CUDA_LAUNCH_BLOCKING=1, or Nsight Compute,
+  // which replays kernels one at a time).
+  static const int la_mode = [] {
+    if (const char* e = getenv("BGP_LOOKAHEAD")) return atoi(e);
+    const char* blocking = getenv("CUDA_LAUNCH_BLOCKING");
+    if ((blocking && atoi(blocking) != 0) || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE")) return 0;
+    return 1;
   }();
-  // after POTRF(K) on stream st: what the panel solve of K needs
-  auto after_potrf = [&](int K, cudaStream_t st) -> int {
-    if (trsm_mode == 0 || K + 1 >= T) return BGP_OK;
-    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st);
-  };
-  // panel solve of K on the caller's stream: L_IK = A_IK L_KK^{-T}, I > K
-  auto panel_solve = [&](int K) -> int {
-    if (K + 1 >= T) return BGP_OK;
-    double* panel = tiles + tri_index(K + 1, K, T) * tsz;
-    if (trsm_mode == 0)
-      return launch_panel_trsm(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, panel, T - K - 1, b, 0, s);
-    GemmProblem p{};
-    p.mode = GEMM_TRSM_PANEL;
-    p.b = b;
-    p.T = T;
-    p.J = K;
-    p.count = T - K - 1;
-    p.panel0 = tri_index(K + 1, K, T);
-    p.alpha = 1.0;
-    p.beta = 0.0;
-    p.check_info = true;
-    return launch_gemm(ctx, p, tiles, tiles, ntiles, ctx->d_linv, 1, ntiles, s);
-  };
-  // profiling: main-stream marks (start, potrf0, trsm0, then gemm / wait / trsm
-  // per step) and side-stream potrf start/end pairs
-  const int nev = 5 * T + 4;
+  // profiling: main-stream marks, side-stream POTRF start/end pairs
+  const int nev = 3 * T + 8;
   if (ctx->profile && ctx->events_cap < nev) {
     for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
     delete[] ctx->events;
@@ -287,63 +276,44 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     if (a >= 0 && c >= 0) cudaEventElapsedTime(&ms, ctx->events[a], ctx->events[c]);
     return (double)ms;
   };
+  // tri_inv of K (needed when panel K has tiles below the diagonal)
+  auto inverse = [&](int K, cudaStream_t st, int* done) -> int {
+    if (K + 1 >= T) return BGP_OK;
+    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st, done,
+                          st == ctx->side);
+  };
+  // standalone panel solve of K on the caller's stream
+  auto panel_solve = [&](int K) -> int {
+    if (K + 1 >= T) return BGP_OK;
+    GemmProblem p{};
+    p.mode = GEMM_TRSM_PANEL;
+    p.b = b;
+    p.T = T;
+    p.J = K;
+    p.count = T - K - 1;
+    p.panel0 = tri_index(K + 1, K, T);
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    p.check_info = true;
+    return launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv);
+  };
   struct StepMarks {
-    int gemm_end, wait_end, trsm_end, p0, p1;
+    int gemm_end, p0, p1, t_end;
   };
   static thread_local StepMarks sm_[4096];
+
   const int m_start = mark(s);
   if ((rc = launch_tile_potrf(ctx, tiles, b, 0, ctx->d_dinv, s))) return rc;
-  if ((rc = after_potrf(0, s))) return rc;
+  if ((rc = inverse(0, s, nullptr))) return rc;
   const int m_p0 = mark(s);
   if ((rc = panel_solve(0))) return rc;
-  int m_prev = mark(s);
-  const int m_t0 = m_prev;
-  // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead; 0 sequential on
-  // all SMs; 2 sequential with the trailing update on all SMs but one.  The
-  // look-ahead POTRF waits on a kernel running concurrently, so it is off
-  // when kernels are serialised (CUDA_LAUNCH_BLOCKING=1, or Nsight Compute,
-  // which replays kernels one at a time).
-  static const int la_mode = [] {
-    if (const char* e = getenv("BGP_LOOKAHEAD")) return atoi(e);
-    const char* blocking = getenv("CUDA_LAUNCH_BLOCKING");
-    if ((blocking && atoi(blocking) != 0) || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE")) return 0;
-    return 1;
-  }();
+  const int m_t0 = mark(s);
+  int m_last = m_t0;
   for (int J = 0; J + 1 < T; ++J) {
     const int K = J + 1;  // next panel
     double* dkk = tiles + tri_index(K, K, T) * tsz;
-    StepMarks sm{-1, -1, -1, -1, -1};
-    if (la_mode != 1) {
-      GemmProblem p{};
-      p.mode = GEMM_CHOL_TRAIL;
-      p.b = b;
-      p.T = T;
-      p.J = J;
-      p.alpha = -1.0;
-      p.beta = 1.0;
-      p.check_info = true;
-      p.grid_limit = la_mode == 2 ? ctx->num_sms - 1 : 0;
-      if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
-      sm.gemm_end = mark(s);
-      sm.p0 = mark(s);
-      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, s))) return rc;
-      if ((rc = after_potrf(K, s))) return rc;
-      sm.p1 = sm.wait_end = mark(s);
-      if ((rc = panel_solve(K))) return rc;
-      sm.trsm_end = mark(s);
-      if (J < 4096) sm_[J] = sm;
-      continue;
-    }
-    // POTRF(K) may start once TRSM(J) released the shared inverse buffer
-    cudaEventRecord(ctx->ev_col, s);
-    cudaStreamWaitEvent(ctx->side, ctx->ev_col, 0);
-    sm.p0 = mark(ctx->side);
-    if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, ctx->side, ctx->d_gate + J,
-                                gate_need)))
-      return rc;
-    if ((rc = after_potrf(K, ctx->side))) return rc;
-    sm.p1 = mark(ctx->side);
-    cudaEventRecord(ctx->ev_fact, ctx->side);
+    int* gate = ctx->d_gate + (int64_t)J * stride;
+    StepMarks sm{-1, -1, -1, -1};
     GemmProblem p{};
     p.mode = GEMM_CHOL_TRAIL;
     p.b = b;
@@ -352,44 +322,83 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     p.alpha = -1.0;
     p.beta = 1.0;
     p.check_info = true;
-    p.grid_limit = ctx->num_sms - 1;  // the spare SM runs POTRF(K)
-    p.signal = ctx->d_gate + J;
-    p.signal_tile = tri_index(K, K, T);
-    if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
-    sm.gemm_end = mark(s);
-    cudaStreamWaitEvent(s, ctx->ev_fact, 0);
-    sm.wait_end = mark(s);
-    if ((rc = panel_solve(K))) return rc;
-    sm.trsm_end = mark(s);
+    p.queue = gate + stride - 2;
+    if (la_mode == 1) {
+      // POTRF(K) + inverse on the side stream once the previous launch (which
+      // read the shared inverse buffers) is done; they run on the spare SM
+      cudaEventRecord(ctx->ev_col, s);
+      cudaStreamWaitEvent(ctx->side, ctx->ev_col, 0);
+      sm.p0 = mark(ctx->side);
+      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, ctx->side, gate, diag_need)))
+        return rc;
+      if ((rc = inverse(K, ctx->side, gate + T))) return rc;
+      sm.p1 = mark(ctx->side);
+      p.grid_limit = ctx->num_sms - 1;
+      p.col_gate = gate;
+      p.trsm_next = (K + 1 < T);
+      p.tile_need = tile_need;
+      p.linv_flag = gate + T;
+      p.linv_need = nbk;
+      p.trsm_tail = 12 * ctx->num_sms;  // ~6 update blocks per consumer group
+      if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
+      sm.gemm_end = mark(s);
+    } else {
+      p.grid_limit = la_mode == 2 ? ctx->num_sms - 1 : 0;
+      if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
+      sm.gemm_end = mark(s);
+      sm.p0 = sm.gemm_end;
+      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, s))) return rc;
+      if ((rc = inverse(K, s, nullptr))) return rc;
+      sm.p1 = mark(s);
+      if ((rc = panel_solve(K))) return rc;
+      sm.t_end = mark(s);
+      if (J < 4096) sm_[J] = sm;
+      m_last = sm.t_end;
+      continue;
+    }
     if (J < 4096) sm_[J] = sm;
+    m_last = sm.gemm_end;
+  }
+  int m_wait = -1;
+  if (la_mode == 1) {  // the last POTRF ran on the side stream
+    cudaEventRecord(ctx->ev_fact, ctx->side);
+    cudaStreamWaitEvent(s, ctx->ev_fact, 0);
+    m_wait = mark(s);
   }
   rc = read_info(ctx, s, info);
   if (rc == BGP_OK && info && (unsigned long long)*info >= BGP_INFO_DATAFLOW_TIMEOUT) {
-    ctx->err = "look-ahead POTRF wait timed out (internal dependency error)";
+    ctx->err = "look-ahead wait timed out (internal dependency error)";
     return BGP_E_CUDA;
   }
   if (rc == BGP_OK && ctx->profile) {
-    ctx->prof[0] += el(m_start, m_p0);  // potrf(0): on the critical path
+    ctx->prof[0] += el(m_start, m_p0);  // potrf(0) + inverse: on the critical path
     ctx->prof[9] += el(m_start, m_p0);
     ctx->prof[5] += 1;
-    ctx->prof[1] += el(m_p0, m_t0);
+    ctx->prof[1] += el(m_p0, m_t0);  // trsm(0)
     ctx->prof[6] += 1;
-    int last = m_t0;
+    int prev = m_t0;
     for (int J = 0; J + 1 < T && J < 4096; ++J) {
       const StepMarks& m = sm_[J];
-      ctx->prof[2] += el(m_prev, m.gemm_end);
-      ctx->prof[3] += 1;
-      ctx->prof[9] += el(m.gemm_end, m.wait_end);
-      ctx->prof[1] += el(m.wait_end, m.trsm_end);
-      ctx->prof[6] += 1;
-      ctx->prof[0] += el(m.p0, m.p1);
-      ctx->prof[5] += 1;
       const double kk = (double)(T - J - 1);
-      ctx->prof[4] += (double)b * b * b * kk * kk;
-      m_prev = m.trsm_end;
-      last = m.trsm_end;
+      if (la_mode == 1) {
+        ctx->prof[2] += el(prev, m.gemm_end);  // update + fused TRSM of the next panel
+        ctx->prof[0] += el(m.p0, m.p1);
+        ctx->prof[4] += (double)b * b * b * (kk * kk + (kk - 1.0));
+        prev = m.gemm_end;
+      } else {
+        ctx->prof[2] += el(prev, m.gemm_end);
+        ctx->prof[0] += el(m.p0, m.p1);
+        ctx->prof[9] += el(m.p0, m.p1);
+        ctx->prof[1] += el(m.p1, m.t_end);
+        ctx->prof[6] += 1;
+        ctx->prof[4] += (double)b * b * b * kk * kk;
+        prev = m.t_end;
+      }
+      ctx->prof[3] += 1;
+      ctx->prof[5] += 1;
     }
-    ctx->prof[8] += el(m_start, last);
+    if (m_wait >= 0) ctx->prof[9] += el(m_last, m_wait);
+    ctx->prof[8] += el(m_start, m_wait >= 0 ? m_wait : m_last);
     ctx->prof[7] += 1;
   }
   return rc;

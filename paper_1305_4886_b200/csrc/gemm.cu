@@ -1,22 +1,26 @@
-// K2c / K3b / K3c: persistent FP64 tensor-core GEMM on packed tiles.
+// K2c / K2b / K3b / K3c: persistent FP64 tensor-core GEMM on packed tiles.
 //
-// Computes, for a list of 128x128 output blocks of b x b column-major tiles,
+// Computes, for a list of 128x64 output blocks of b x b column-major tiles,
 //     D = beta * C + alpha * sum_k A(m, k) B(n, k)        (A, B "MN-major")
 // which covers
 //   * the Cholesky trailing SYRK/GEMM   A_RC -= L_RJ L_CJ^T
 //     (bg/distla/kernels.py:188-192, ~all of the n^3/3 flops),
+//   * the panel TRSM                    L_IJ = A_IJ L_JJ^-T = A_IJ Linv^T
+//     (kernels.py:163-164), in place, 64 columns at a time right to left,
 //   * the kriging multi-RHS update      B^T_I -= X^T_J L_IJ^T
 //     (solve_rect partial GEMMs, kernels.py:287-291),
 //   * the crossproduct                  S = V^T V   (xprod_self, kernels.py:448).
 //
 // sm_100a has no FP64 tcgen05 kind, so the MMA is mma.sync m8n8k4 f64
 // (SASS DMMA.8x8x4, 128 flop/clk/SM).  Operands are staged by TMA
-// (cp.async.bulk.tensor, 128B swizzle) into a 4-stage mbarrier ring filled by
-// one producer warp; 8 MMA warps each own a 64x32 accumulator (64 FP64 regs).
-// The C block is TMA-loaded into shared memory during the main loop and the
-// result is TMA-stored from the same buffer, so the epilogue's HBM traffic
-// overlaps the next block's main loop.  One CTA per SM, static round-robin
-// over blocks (all blocks have equal cost).
+// (cp.async.bulk.tensor, 128B swizzle) into per-group mbarrier rings; results
+// leave through shared memory by TMA store or TMA reduce-add (C += -acc in
+// L2).  One CTA per SM.  Work is a queue of tasks claimed with an atomic
+// counter by each group's producer warp, which hands the block id to its
+// consumers through the ring (dynamic scheduling: no static imbalance).
+// A trailing-update launch can append the TRSM of the next panel as tasks:
+// their producer waits, per tile, until the update blocks of that tile have
+// retired and the side stream published the tile inverse.
 //
 // Bank conflicts: a 16-double-wide TMA box with 128B swizzle stores element
 // (mn, k) at chunk ((mn&15)>>1) ^ (k&7).  Each MMA k4 step takes
@@ -54,7 +58,7 @@ constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;  // 32 KB per group
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
-constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
+constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 #ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
@@ -63,13 +67,16 @@ __device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][3];
 #endif
 
 struct Item {
-  int64_t cTile, aTile0, bTile0;
+  int cTile, aTile0, bTile0;  // tile indices (< 2^31: 1.4e5 tiles at n = 131,072, b = 256)
   int bTriRow;               // >= 0: B tile for k tile kt is L(bTriRow, kt) (TRMM)
-  int64_t aStride, bStride;  // tile-index stride per k tile
+  int aStride, bStride;      // tile-index stride per k tile
   int nkt;                   // number of k tiles
   int mrow0, nrow0;          // row offsets inside the A / B tiles (= C block offsets)
   int lower;                 // block straddles the diagonal of a diagonal tile
   int kstages;               // > 0: number of BK stages (triangular k range), else nkt * b / BK
+  int store;                 // 1: TMA store of acc (beta = 0 / TRSM), 0: reduce-add of -acc
+  int bLinv;                 // 1: B operand from the Linv map (fused TRSM block)
+  int gate;                  // >= 0: column-gate index this block signals (update of column J+1)
   bool valid;
 };
 
@@ -77,11 +84,9 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
   const int nblk = (p.b / BM) * (p.b / BN);
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
-      const int64_t k = p.T - p.J - 1 - p.coff;
+      const int64_t k = p.T - p.J - 1;
       return k > 0 ? k * (k + 1) / 2 * nblk : 0;
     }
-    case GEMM_CHOL_COL:
-      return (int64_t)(p.T - p.J - 1) * nblk;
     case GEMM_RECT_TRAIL:
       return (int64_t)p.Tm * (p.T - p.J - 1) * nblk;
     case GEMM_SYRK_RECT:
@@ -93,11 +98,51 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
   }
 }
 
-// blocks of one task that the same consumer group must run back to back
-// (TRSM: the column blocks of a 128-row slab, right to left, so the in-place
-// solve never overwrites columns a later block still reads)
-__host__ __device__ __forceinline__ int gemm_passes(const GemmProblem& p) {
-  return p.mode == GEMM_TRSM_PANEL ? p.b / BN : 1;
+// Tasks: a task is claimed by one consumer group and runs its blocks back to
+// back.  Plain modes: one block per task.  TRSM (standalone, or appended to a
+// trailing update for the next panel): a 128-row slab of a panel tile, its
+// b/64 column blocks right to left, so the in-place solve never overwrites
+// columns a later block still reads.
+__host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p) {
+  if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM);
+  if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next) return (int64_t)(p.T - p.J - 2) * (p.b / BM);
+  return 0;
+}
+// Queue position of the fused TRSM tasks in a trailing-update launch: after
+// every block of tile column J+1 (their inputs) and early enough that the
+// last ~trsm_tail update blocks, small and uniform, fill the launch's tail
+// instead of the large TRSM tasks.
+__host__ __device__ __forceinline__ int64_t gemm_trsm_pos(const GemmProblem& p) {
+  const int64_t nupd = gemm_num_items(p);
+  const int64_t col = (int64_t)(p.T - p.J - 1) * (p.b / BM) * (p.b / BN);
+  const int64_t pos = nupd - p.trsm_tail;
+  return pos > col ? pos : (col < nupd ? col : nupd);
+}
+// task -> (is TRSM, index among its kind)
+__host__ __device__ __forceinline__ bool gemm_task_kind(const GemmProblem& p, int64_t task, int64_t& idx) {
+  if (p.mode == GEMM_TRSM_PANEL) {
+    idx = task;
+    return true;
+  }
+  if (p.mode != GEMM_CHOL_TRAIL || !p.trsm_next) {
+    idx = task;
+    return false;
+  }
+  const int64_t pos = gemm_trsm_pos(p), ntrsm = gemm_trsm_tasks(p);
+  if (task < pos) {
+    idx = task;
+    return false;
+  }
+  if (task < pos + ntrsm) {
+    idx = task - pos;
+    return true;
+  }
+  idx = task - ntrsm;
+  return false;
+}
+
+__host__ __device__ __forceinline__ int64_t gemm_num_tasks(const GemmProblem& p) {
+  return p.mode == GEMM_TRSM_PANEL ? gemm_trsm_tasks(p) : gemm_num_items(p) + gemm_trsm_tasks(p);
 }
 
 // diagonal-tile block (bi, bj): skip blocks strictly above the diagonal,
@@ -107,57 +152,63 @@ __device__ __forceinline__ void diag_block(Item& it, int bi, int bj) {
   it.lower = (bi * BM < bj * BN + BN - 1);
 }
 
-__device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) {
+// TRSM block: slab task `task` (tile task / nbm, rows (task % nbm) * BM) of
+// the panel starting at tile index panel0, column block pass-th from the right
+__device__ __forceinline__ void trsm_block(Item& it, const GemmProblem& p, int64_t task, int pass,
+                                           int64_t panel0) {
+  const int nbn = p.b / BN, nbm = p.b / BM;
+  const int bjj = nbn - 1 - pass;
+  it.mrow0 = (int)(task % nbm) * BM;
+  it.nrow0 = bjj * BN;
+  it.cTile = it.aTile0 = (int)(panel0 + task / nbm);
+  it.bTile0 = 0;                     // Linv (single tile)
+  it.kstages = (bjj + 1) * BN / BK;  // Linv(n, k) = 0 for k > n
+  it.store = 1;
+  it.bLinv = 1;
+}
+
+// Block `pass` of task `task`.
+__device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, int pass) {
   const int nbn = p.b / BN;
   const int nblk = (p.b / BM) * nbn;
-  const int64_t t = item / nblk;
-  const int blk = (int)(item % nblk);
-  const int bi = blk / nbn, bj = blk % nbn;
   Item it;
-  it.mrow0 = bi * BM;
-  it.nrow0 = bj * BN;
   it.aStride = it.bStride = 0;
   it.nkt = 1;
   it.valid = true;
   it.lower = 0;
   it.bTriRow = -1;
   it.kstages = 0;
+  it.store = (p.beta == 0.0);
+  it.bLinv = 0;
+  it.gate = -1;
+  int64_t idx;
+  if (gemm_task_kind(p, task, idx)) {
+    // standalone panel, or the fused TRSM of panel J+1 (tiles J+2 .. T-1)
+    trsm_block(it, p, idx, pass, p.mode == GEMM_TRSM_PANEL ? p.panel0 : tri_index(p.J + 2, p.J + 1, p.T));
+    return it;
+  }
+  const int64_t t = idx / nblk;
+  const int blk = (int)(idx % nblk);
+  const int bi = blk / nbn, bj = blk % nbn;
+  it.mrow0 = bi * BM;
+  it.nrow0 = bj * BN;
   switch (p.mode) {
-    case GEMM_TRSM_PANEL: {  // item = task * nbn + pass, task = tile * (b/BM) + row block
-      const int pass = (int)(item % nbn);
-      const int64_t task = item / nbn;
-      const int nbm = p.b / BM;
-      const int bjj = nbn - 1 - pass;
-      it.mrow0 = (int)(task % nbm) * BM;
-      it.nrow0 = bjj * BN;
-      it.cTile = it.aTile0 = p.panel0 + task / nbm;
-      it.bTile0 = 0;                     // Linv (single tile)
-      it.kstages = (bjj + 1) * BN / BK;  // Linv(n, k) = 0 for k > n
-      break;
-    }
     case GEMM_CHOL_TRAIL: {
       int rr, cc;
-      tri_decode(t, p.T - p.J - 1 - p.coff, rr, cc);
-      const int R = p.J + 1 + p.coff + rr, C = p.J + 1 + p.coff + cc;
+      tri_decode(t, p.T - p.J - 1, rr, cc);
+      const int R = p.J + 1 + rr, C = p.J + 1 + cc;
       it.cTile = tri_index(R, C, p.T);
       it.aTile0 = tri_index(R, p.J, p.T);
       it.bTile0 = tri_index(C, p.J, p.T);
       if (R == C) diag_block(it, bi, bj);
-      break;
-    }
-    case GEMM_CHOL_COL: {
-      const int R = p.J + 1 + (int)t, C = p.J + 1;
-      it.cTile = tri_index(R, C, p.T);
-      it.aTile0 = tri_index(R, p.J, p.T);
-      it.bTile0 = tri_index(C, p.J, p.T);
-      if (R == C) diag_block(it, bi, bj);
+      if (cc == 0 && p.col_gate) it.gate = rr;  // column J+1: POTRF / TRSM of the next panel wait on it
       break;
     }
     case GEMM_RECT_TRAIL: {
       const int a = (int)(t % p.Tm);
       const int I = p.J + 1 + (int)(t / p.Tm);
-      it.cTile = (int64_t)I * p.Tm + a;
-      it.aTile0 = (int64_t)p.J * p.Tm + a;
+      it.cTile = I * p.Tm + a;
+      it.aTile0 = p.J * p.Tm + a;
       it.bTile0 = tri_index(I, p.J, p.T);
       break;
     }
@@ -175,7 +226,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
     case GEMM_TRMM_RECT: {  // Y^T(a, I) = sum_{J <= I} X^T(a, J) L(I, J)^T
       const int a = (int)(t % p.Tm);
       const int I = (int)(t / p.Tm);
-      it.cTile = (int64_t)I * p.Tm + a;
+      it.cTile = I * p.Tm + a;
       it.aTile0 = a;
       it.aStride = p.Tm;
       it.nkt = I + 1;
@@ -195,6 +246,24 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t item) 
   return it;
 }
 
+__device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
+  int64_t idx;
+  return gemm_task_kind(p, task, idx) ? p.b / BN : 1;
+}
+
+// spin (acquire, exponential back-off, bounded) until *flag >= need or the
+// factorization failed; returns false on failure / timeout
+__device__ __forceinline__ bool wait_count(const int* flag, int need, const unsigned long long* info) {
+  unsigned ns = 32;
+  for (long long spins = 0; ld_acquire_gpu(flag) < need; ++spins) {
+    if (info && *(volatile const unsigned long long*)info != 0ull) return false;
+    if (spins > (1ll << 24)) return false;
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
+  return true;
+}
+
 // Per-lane byte offset of MMA fragment element (row p*8 + q of a 16-row TMA
 // box, k = 2*s4 + t, t = 0, 1) inside a 128B-swizzled box whose 128-byte
 // lines are k (operands) or n (C buffer):
@@ -211,6 +280,7 @@ struct GroupSmem {
   uint8_t* cbuf;
   uint64_t* full;
   uint64_t* empty;
+  int64_t* slot;  // per stage: block id (task * 64 + pass) starting there, -1: no more work
 };
 
 __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
@@ -220,6 +290,7 @@ __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES);
   gs.full = bars;
   gs.empty = bars + STAGES;
+  gs.slot = reinterpret_cast<int64_t*>(bars + GROUPS * 2 * STAGES + 1 - g * (2 * STAGES)) + g * STAGES;
   return gs;
 }
 
@@ -227,56 +298,73 @@ __device__ __forceinline__ uint64_t* stagger_bar(uint8_t* smem) {
   return reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + GROUPS * 2 * STAGES;
 }
 
-__device__ __forceinline__ void producer_loop(const GroupSmem& gs, int g, const CUtensorMap* tmA,
-                                              const CUtensorMap* tmB, const CUtensorMap* tmC,
-                                              const GemmProblem& p, int64_t nitems) {
-#ifdef BGP_EXP_NO_BAR
-  return;
-#endif
+__device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtensorMap* tmA,
+                                              const CUtensorMap* tmB, const CUtensorMap* tmL,
+                                              const CUtensorMap* tmC, const GemmProblem& p,
+                                              const unsigned long long* info, uint64_t* stagger) {
   prefetch_tmap(tmA);
   prefetch_tmap(tmB);
+  prefetch_tmap(tmL);
   prefetch_tmap(tmC);
   const uint64_t pol_keep = l2_policy_evict_last();
   const int kc_per_tile = p.b / BK;
+  const int64_t ntasks = gemm_num_tasks(p);
   int stage = 0;
   uint32_t phase = 0;
-  const int npass = gemm_passes(p);
-  for (int64_t task = blockIdx.x + (int64_t)g * gridDim.x; task * npass < nitems;
-       task += (int64_t)GROUPS * gridDim.x)
-  for (int pass = 0; pass < npass; ++pass) {
-    const Item it = gemm_decode(p, task * npass + pass);
-    if (!it.valid) continue;
-    const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
-    for (int kc = 0; kc < nk; ++kc) {
-      mbar_wait(&gs.empty[stage], phase ^ 1);
-#ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
-      mbar_arrive(&gs.full[stage]);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1;
+  for (;;) {
+    const int64_t task = atomicAdd(reinterpret_cast<unsigned long long*>(p.queue), 1ull);
+    if (task >= ntasks) break;
+    int64_t idx;
+    if (p.mode == GEMM_CHOL_TRAIL && gemm_task_kind(p, task, idx)) {
+      // fused TRSM of panel J+1: the tile's column-(J+1) update blocks have
+      // retired and the side stream published Linv(J+1)
+      const int tile = (int)(idx / (p.b / BM));
+      if (stagger) {  // group 0: release group 1 before blocking (see consumer_loop)
+        mbar_arrive(stagger);
+        stagger = nullptr;
       }
-      continue;
+      if (!wait_count(p.col_gate + 1 + tile, p.tile_need, info) || !wait_count(p.linv_flag, p.linv_need, info))
+        break;
+      fence_proxy_async_global();
+    }
+    const int npass = gemm_task_passes(p, task);
+    for (int pass = 0; pass < npass; ++pass) {
+      const Item it = gemm_decode(p, task, pass);
+      if (!it.valid) continue;
+      const CUtensorMap* tb = it.bLinv ? tmL : tmB;
+      const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&gs.empty[stage], phase ^ 1);
+        if (kc == 0) gs.slot[stage] = task * 64 + pass;  // read by the consumers after `full`
+#ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
+        mbar_arrive(&gs.full[stage]);
+#else
+        mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
+        const int kt = kc / kc_per_tile;
+        const int kin = (kc % kc_per_tile) * BK;
+        const int at = (int)(it.aTile0 + kt * it.aStride);
+        const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, p.T)
+                                       : (int)(it.bTile0 + kt * it.bStride);
+        uint8_t* sa = gs.stages + stage * STAGE_BYTES;
+        uint8_t* sb = sa + STAGE_A_BYTES;
+#pragma unroll
+        for (int i = 0; i < BM / 16; ++i)
+          tma_load_3d(sa + i * BOX_BYTES, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i)
+          tma_load_3d(sb + i * BOX_BYTES, tb, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
 #endif
-      mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
-      const int kt = kc / kc_per_tile;
-      const int kin = (kc % kc_per_tile) * BK;
-      const int at = (int)(it.aTile0 + kt * it.aStride);
-      const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, p.T)
-                                     : (int)(it.bTile0 + kt * it.bStride);
-      uint8_t* sa = gs.stages + stage * STAGE_BYTES;
-      uint8_t* sb = sa + STAGE_A_BYTES;
-#pragma unroll
-      for (int i = 0; i < BM / 16; ++i)
-        tma_load_3d(sa + i * BOX_BYTES, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
-#pragma unroll
-      for (int i = 0; i < BN / 16; ++i)
-        tma_load_3d(sb + i * BOX_BYTES, tmB, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1;
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
     }
   }
+  // no more work: hand the consumers a sentinel through the next stage
+  mbar_wait(&gs.empty[stage], phase ^ 1);
+  gs.slot[stage] = -1;
+  mbar_arrive(&gs.full[stage]);
 }
 
 // ld.shared.f64 at a register base plus an immediate; volatile so it keeps
@@ -357,9 +445,8 @@ __device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const
   }
 }
 
-template <bool ACC>
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
-                                              const CUtensorMap* tmC, const GemmProblem& p, int64_t nitems,
+                                              const CUtensorMap* tmC, const GemmProblem& p,
                                               uint64_t* stagger) {
   static_assert(MI == 8 && NJ == 4 && WM / 16 == 4 && WN / 16 == 2, "load_frag assumes a 64x32 warp tile");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
@@ -387,18 +474,21 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   const uint64_t pol_stream = l2_policy_evict_first();
   // Stagger: every block costs the same, so two groups that start together
   // would hit their epilogues together and leave the DMMA pipe idle.  Group 1
-  // starts once group 0 is half-way through its first block (group 0 always
-  // arrives exactly once, also when it has no block at all).
-  bool stagger_arrive = (g == 0);
+  // starts once group 0 is half-way through its first block.  The barrier
+  // (count 1) also completes when group 0 has no block at all, and when group
+  // 0's producer is about to wait on a gate, so group 1 never waits on a
+  // group that itself waits (the gated work may be group 1's own).
+  bool stagger_arrive = (g == 0 && gwarp == 0);
   if (g == 1) mbar_wait(stagger, 0);
+#ifdef BGP_EXP_TRACE
+  int t_idx = 0;
+#endif
 
-  const int npass = gemm_passes(p);
-  for (int64_t task = blockIdx.x + (int64_t)g * gridDim.x; task * npass < nitems;
-       task += (int64_t)GROUPS * gridDim.x)
-  for (int pass = 0; pass < npass; ++pass) {
-    const int64_t item = task * npass + pass;
-    const Item it = gemm_decode(p, item);
-    if (!it.valid) continue;
+  for (;;) {
+    mbar_wait(&gs.full[stage], phase);  // first stage of the next block (or the sentinel)
+    const int64_t slot = gs.slot[stage];
+    if (slot < 0) break;
+    const Item it = gemm_decode(p, slot >> 6, (int)(slot & 63));
     const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
     double acc[MI][NJ][2];
 #pragma unroll
@@ -412,7 +502,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     // wait for stage s+1 sits before the last half-step of stage s, and
     // stage s is released once its last DMMA issued (fragments in registers).
 #ifdef BGP_EXP_TRACE
-    const int t_idx = (int)((item - blockIdx.x) / ((int64_t)GROUPS * gridDim.x));
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][0] = clock64();
 #endif
@@ -420,9 +509,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     uint32_t sb = (uint32_t)stage * STAGE_BYTES;
 #define BGP_LOAD(F, H) load_frag<((H) >> 1)>(F, offA[0][(H) & 1] + sb, offA[1][(H) & 1] + sb, \
                                              offB[0][(H) & 1] + sb, offB[1][(H) & 1] + sb)
-#ifndef BGP_EXP_NO_BAR
-    mbar_wait(&gs.full[stage], phase);
-#endif
     BGP_LOAD(x, 0);
     for (int kc = 0; kc + 1 < nk; ++kc) {
       const int cur = stage;
@@ -442,15 +528,11 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         phase ^= 1;
       }
       sb = (uint32_t)stage * STAGE_BYTES;
-#ifndef BGP_EXP_NO_BAR
       mbar_wait(&gs.full[stage], phase);
-#endif
       BGP_LOAD(x, 0);
       mma_frag(acc, y);
-#ifndef BGP_EXP_NO_BAR
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[cur]);
-#endif
     }
     BGP_LOAD(y, 1);
     mma_frag(acc, x);
@@ -460,10 +542,8 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     mma_frag(acc, x);
     mma_frag(acc, y);
 #undef BGP_LOAD
-#ifndef BGP_EXP_NO_BAR
     __syncwarp();
     if (lane == 0) mbar_arrive(&gs.empty[stage]);
-#endif
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
@@ -471,11 +551,15 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 
     // ------------------------------- epilogue -------------------------------
     // Per warp (no group barrier), in two rounds of 32 rows: stage the rows in
-    // the warp's own 8 KB slice and issue two 16x32 TMA boxes.  beta = 1
-    // (updates): stage -acc and TMA reduce-add it into C in L2 -- no C load,
-    // no read-modify-write on the critical path.  beta = 0 (V^T V, L X): TMA
-    // store of acc.  A round waits only until the previous round's boxes
-    // were read out of shared memory.
+    // the warp's own 8 KB slice and issue two 16x32 TMA boxes.  Updates
+    // (beta = 1): stage -acc and TMA reduce-add it into C in L2 -- no C load,
+    // no read-modify-write on the critical path.  Stores (beta = 0, TRSM
+    // blocks): TMA store of acc.  A round waits only until the previous
+    // round's boxes were read out of shared memory.
+#ifdef BGP_EXP_TRACE
+    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+      g_trace[blockIdx.x][g][t_idx][1] = clock64();
+#endif
 #ifdef BGP_EXP_NO_EPI  // probe build: no epilogue
     {
       double sum = 0.0;
@@ -487,22 +571,28 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     }
     continue;
 #endif
-#ifdef BGP_EXP_TRACE
-    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-      g_trace[blockIdx.x][g][t_idx][1] = clock64();
-#endif
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       if (lane == 0 && (store_pending || r == 1)) tma_store_wait_read0();  // slice free again
       __syncwarp();
       // row m = m0 + ii*8 of the round, column n = n0 + j*8 + e (tile coordinates)
       const int m0 = it.mrow0 + wm * WM + r * (WM / 2) + q, n0 = it.nrow0 + wn * WN + 2 * s4;
-      if (it.lower) {
-        if (r == 0) stage_rows<0, ACC, true>(acc, cbase, m0, n0);
-        else stage_rows<1, ACC, true>(acc, cbase, m0, n0);
+      if (it.store) {
+        if (it.lower) {
+          if (r == 0) stage_rows<0, false, true>(acc, cbase, m0, n0);
+          else stage_rows<1, false, true>(acc, cbase, m0, n0);
+        } else {
+          if (r == 0) stage_rows<0, false, false>(acc, cbase, m0, n0);
+          else stage_rows<1, false, false>(acc, cbase, m0, n0);
+        }
       } else {
-        if (r == 0) stage_rows<0, ACC, false>(acc, cbase, m0, n0);
-        else stage_rows<1, ACC, false>(acc, cbase, m0, n0);
+        if (it.lower) {
+          if (r == 0) stage_rows<0, true, true>(acc, cbase, m0, n0);
+          else stage_rows<1, true, true>(acc, cbase, m0, n0);
+        } else {
+          if (r == 0) stage_rows<0, true, false>(acc, cbase, m0, n0);
+          else stage_rows<1, true, false>(acc, cbase, m0, n0);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -510,42 +600,41 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         const int r0 = it.mrow0 + wm * WM + r * (WM / 2), c0 = it.nrow0 + wn * WN;
 #pragma unroll
         for (int b2 = 0; b2 < 2; ++b2) {
-          if (ACC)
-            tma_reduce_add_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
-          else
+          if (it.store)
             tma_store_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+          else
+            tma_reduce_add_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
         }
         tma_store_commit();
       }
     }
     store_pending = true;
-    if (p.signal && it.cTile == p.signal_tile) {
-      // look-ahead: the next panel's diagonal tile is complete once every warp
-      // that reduces into it has its bulk ops retired
+    // Column-(J+1) gates: a warp signals a block once its bulk reduction has
+    // retired (completion, proxy fence, release).  Not deferred: this group's
+    // own producer may be the one waiting for the tile.
+    if (it.gate >= 0) {
       if (lane == 0) {
         tma_store_wait_all0();
         fence_proxy_async_global();
         __threadfence();
-        atomicAdd(p.signal, 1);
+        atomicAdd(p.col_gate + it.gate, 1);
       }
       __syncwarp();
     }
 #ifdef BGP_EXP_TRACE
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][2] = clock64();
+    ++t_idx;
 #endif
   }
-  if (stagger_arrive) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(stagger);
-  }
+  if (stagger_arrive && lane == 0) mbar_arrive(stagger);
   if (lane == 0 && store_pending) tma_store_wait_all0();
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const GemmProblem p,
-                     const unsigned long long* __restrict__ info) {
+                     const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmC,
+                     const GemmProblem p, const unsigned long long* __restrict__ info) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
   if (info && *(volatile const unsigned long long*)info != 0ull) return;  // factorization failed
@@ -560,24 +649,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(&gs.empty[s], GROUP_WARPS);
       }
     }
-    mbar_init(stagger_bar(smem), GROUP_WARPS);
+    mbar_init(stagger_bar(smem), 1);
     fence_barrier_init();
   }
   __syncthreads();
 
-  const int64_t nitems = gemm_num_items(p);
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (warp < GROUPS && lane == 0)
-      producer_loop(group_smem(smem, warp), warp, &tmA, &tmB, &tmC, p, nitems);
+      producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmC, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     const int g = wg - 1;
-    // (alpha, beta) = (-1, 1): C -= A B^T by reduce-add;  (1, 0): C = A B^T
-    if (p.beta != 0.0)
-      consumer_loop<true>(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, stagger_bar(smem));
-    else
-      consumer_loop<false>(group_smem(smem, g), g, warp & 3, lane, &tmC, p, nitems, stagger_bar(smem));
+    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem));
   }
 }
 
@@ -594,21 +678,28 @@ void gemm_prepare() {
   }
 }
 
-int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
-                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s) {
-  if (p.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
-  const int64_t items = gemm_num_items(p);
-  if (items <= 0) return BGP_OK;
-  CUtensorMap mA, mB, mC;
+int launch_gemm(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase, int64_t nA,
+                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
+  if (p_in.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
+  GemmProblem p = p_in;
+  const int64_t tasks = gemm_num_tasks(p);
+  if (tasks <= 0) return BGP_OK;
   int rc;
+  if (!p.queue) {  // a zeroed task counter of the context's own
+    if ((rc = ensure(ctx, (void**)&ctx->d_queue, &ctx->queue_cap, 256))) return rc;
+    cudaError_t e = cudaMemsetAsync(ctx->d_queue, 0, 8, s);
+    if (e != cudaSuccess) return set_err(ctx, "gemm queue reset", e);
+    p.queue = ctx->d_queue;
+  }
+  CUtensorMap mA, mB, mL, mC;
   if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
+  if ((rc = make_tile_map(ctx, &mL, Linv ? Linv : Bbase, p.b, Linv ? 1 : nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
   gemm_prepare();
   const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
-  const int64_t tasks = items / gemm_passes(p);
-  const int64_t grid = tasks < slots ? tasks : slots;
-  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mC, p,
+  const int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
+  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
                                                                   p.check_info ? ctx->d_info : nullptr);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");

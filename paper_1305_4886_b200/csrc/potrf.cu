@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
 // shared memory.  Feeds the panel TRSM on the DMMA GEMM (X = A Linv^T).
 __global__ void __launch_bounds__(256) tri_inv_kernel(const double* __restrict__ L,
                                                       const double* __restrict__ dinv, int b,
-                                                      double* __restrict__ Linv) {
+                                                      double* __restrict__ Linv, int* __restrict__ done) {
   extern __shared__ double xs[];  // Linv blocks (i, j), i >= j: [(i-j)*32 + r]*33 + c
   double* tmp = xs + (size_t)(b / NB) * NB * 33;  // 32 x 33
   const int j = blockIdx.x, nbk = b / NB;
@@ -294,6 +294,82 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const double* __restrict__
     const int blk = row / NB;
     const double v = (blk < j) ? 0.0 : xs[((size_t)(blk - j) * NB + (row & 31)) * 33 + c];
     Linv[(int64_t)(j * NB + c) * b + row] = v;
+  }
+  if (done) {  // publish: the fused panel TRSM of the trailing update waits for all column blocks
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(done, 1);
+  }
+}
+
+// Single-CTA inverse of a factored diagonal tile for the look-ahead stream
+// (where only one SM is free): Linv = L^{-1} by block diagonals.  Diagonal
+// d holds the blocks (j + d, j); each is
+//   Linv[j+d][j] = -Dinv_{j+d} * sum_{m=j}^{j+d-1} L[j+d][m] Linv[m][j]
+// and only needs diagonals < d, so all blocks of a diagonal are independent.
+// Both products run on DMMA with fragments loaded from L2 (the tile was just
+// factored); the partial sums of a diagonal are staged in shared memory.
+constexpr int TINV_THREADS = 512;
+__global__ void __launch_bounds__(TINV_THREADS, 1)
+    tri_inv_diag_kernel(const double* __restrict__ L, const double* __restrict__ dinv, int b,
+                        double* __restrict__ Linv, int* __restrict__ done) {
+  extern __shared__ double S[];  // diagonal partial sums: block j at [(j*32 + r)*33 + c]
+  const int nbk = b / NB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nw = TINV_THREADS / 32;
+  const int q = lane >> 2, s4 = lane & 3;
+  // block diagonal = Dinv, strictly upper blocks = 0 (below is written per diagonal)
+  for (int idx = tid; idx < b * b; idx += TINV_THREADS) {
+    const int c = idx / b, r = idx % b;
+    const int bi = r / NB, bj = c / NB;
+    if (bi < bj) Linv[idx] = 0.0;
+    else if (bi == bj) Linv[idx] = dinv[(int64_t)bj * NB * NB + (c % NB) * NB + (r % NB)];
+  }
+  __syncthreads();
+  for (int d = 1; d < nbk; ++d) {
+    const int nblocks = nbk - d;
+    // S_j = sum_m L[j+d][m] Linv[m][j]: one 8x8 output tile per warp task
+    for (int t = warp; t < nblocks * 16; t += nw) {
+      const int j = t >> 4, tr = (t >> 2) & 3, tc = t & 3, i = j + d;
+      double c0 = 0.0, c1 = 0.0;
+      for (int m = j; m < i; ++m) {
+        const double* La = L + (int64_t)(m * NB + s4) * b + i * NB + tr * 8 + q;      // A[q][k] = L[row][32m+k]
+        const double* Lb = Linv + (int64_t)(j * NB + tc * 8 + q) * b + m * NB + s4;  // B[k][q] = Linv[32m+k][col]
+        double av[8], bv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          av[k] = __ldcg(La + (int64_t)(4 * k) * b);
+          bv[k] = __ldcg(Lb + 4 * k);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dmma884(c0, c1, av[k], bv[k]);
+      }
+      double* Sj = S + (size_t)(j * NB + tr * 8 + q) * 33 + tc * 8 + 2 * s4;
+      Sj[0] = c0;
+      Sj[1] = c1;
+    }
+    __syncthreads();
+    // Linv[j+d][j] = -Dinv_{j+d} S_j
+    for (int t = warp; t < nblocks * 16; t += nw) {
+      const int j = t >> 4, tr = (t >> 2) & 3, tc = t & 3, i = j + d;
+      const double* Di = dinv + (int64_t)i * NB * NB;  // column-major 32x32
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double a = Di[(4 * k + s4) * NB + tr * 8 + q];
+        const double bb = S[(size_t)(j * NB + 4 * k + s4) * 33 + tc * 8 + q];
+        dmma884(c0, c1, a, bb);
+      }
+      const int row = i * NB + tr * 8 + q, col = j * NB + tc * 8 + 2 * s4;
+      Linv[(int64_t)col * b + row] = -c0;
+      Linv[(int64_t)(col + 1) * b + row] = -c1;
+    }
+    __syncthreads();
+  }
+  if (done) {  // publish: the fused panel TRSM of the trailing update waits for this
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(done, nbk);
   }
 }
 
@@ -409,6 +485,7 @@ void potrf_prepare() {
     cudaFuncSetAttribute(tile_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, diag_inv_kernel);
     done = true;
@@ -424,9 +501,16 @@ int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv,
   return check_launch(ctx, "tile_potrf");
 }
 
-int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s) {
+int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
+                   int* done, bool one_cta) {
+  if (one_cta) {
+    const size_t smem = (size_t)(b / NB - 1) * NB * 33 * sizeof(double);
+    tri_inv_diag_kernel<<<1, TINV_THREADS, smem > 0 ? smem : 8, s>>>(Ltile, dinv, b, Linv, done);
+    ctx->launches++;
+    return check_launch(ctx, "tri_inv_diag");
+  }
   const size_t smem = ((size_t)(b / NB) * NB * 33 + NB * 33) * sizeof(double);
-  tri_inv_kernel<<<b / NB, 256, smem, s>>>(Ltile, dinv, b, Linv);
+  tri_inv_kernel<<<b / NB, 256, smem, s>>>(Ltile, dinv, b, Linv, done);
   ctx->launches++;
   return check_launch(ctx, "tri_inv");
 }

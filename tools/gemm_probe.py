@@ -18,8 +18,8 @@ from paper_1305_4886_b200 import _lib  # noqa: E402
 
 
 def main():
-    b = 256
-    T = int(os.environ.get("PROBE_T", "96"))
+    b = int(os.environ.get("PROBE_B", "256"))
+    T = int(os.environ.get("PROBE_T", str(96 * 256 // b)))
     reps = int(os.environ.get("PROBE_REPS", "5"))
     dev = torch.device("cuda:0")
     nt = T * (T + 1) // 2
