@@ -107,7 +107,13 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
  * replaces distla.cholesky / _cholesky_sweep (bg/distla/kernels.py:110-194),
  * in place on packed tiles.  info = 0 on success, else the 1-based global
  * row of the first non-positive pivot (LAPACK potrf convention); the caller
- * maps it to NotPositiveDefinite(block) with its layout (kernels.py:146-148). */
+ * maps it to NotPositiveDefinite(block) with its layout (kernels.py:146-148).
+ * The schedule has a one-panel look-ahead: the next panel's tile POTRF and
+ * inverse run on a context-owned side stream (one SM) under the trailing
+ * update, which also solves the next panel; the side
+ * stream is joined into `stream` before the status read.  BGP_LOOKAHEAD=0
+ * in the environment (automatic under CUDA_LAUNCH_BLOCKING=1 or Nsight
+ * Compute) runs the same kernels one after another on `stream`. */
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile,
               int64_t* info, void* stream);
 
