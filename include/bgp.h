@@ -193,6 +193,10 @@ int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out,
  * bgp_tile_update: C -= A B^T over a list of `count` (C, A, B) tile index
  *   triples into three packed-tile bases (kernels.py:188-192); a triple with
  *   lower != 0 updates only the lower triangle (diagonal SYRK). */
+/* bgp_tile_potrf_inv: bgp_tile_potrf (row0 = 0) followed by the one-CTA
+ * inverse the look-ahead uses: linv (b x b column-major) = L^{-1}. */
+int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv,
+                       int64_t* info, void* stream);
 int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0,
                    int64_t* info, void* stream);
 /* A rank's share of construct: lower tiles (I, J) listed in tile_ij (device,
@@ -236,6 +240,9 @@ int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
 #define BGP_PROFILE_SLOTS 10
 int bgp_set_profiling(bgp_ctx_t ctx, int on);
 int bgp_profile_read(bgp_ctx_t ctx, double* out);
+/* per-step trailing-update launch times (ms) of the last profiled bgp_potrf;
+ * returns the number written (<= max) */
+int bgp_profile_steps(bgp_ctx_t ctx, double* out, int max);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ SIGNATURES = {
     "bgp_tri_diagonal": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _c_dp]),
     "bgp_sub": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _i64, _c_dp]),
     "bgp_tile_potrf": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, ctypes.POINTER(_i64), _c_dp]),
+    "bgp_tile_potrf_inv": (_int, [ctypes.c_void_p, _c_dp, _int, _c_dp, ctypes.POINTER(_i64), _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_construct_tiles": (_int, [ctypes.c_void_p, ctypes.POINTER(Generator), _c_dp, _i64, _int, _int,
@@ -76,6 +77,7 @@ SIGNATURES = {
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), _c_dp]),
     "bgp_set_profiling": (_int, [ctypes.c_void_p, _int]),
     "bgp_profile_read": (_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "bgp_profile_steps": (_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _int]),
 }
 
 _LIB = None

@@ -49,6 +49,8 @@ struct Ctx {
   cudaEvent_t* events = nullptr;
   int events_cap = 0;
   double prof[BGP_PROFILE_SLOTS] = {};
+  double step_ms[4096] = {};  // per-step update-launch time of the last profiled factorization
+  int nsteps = 0;
   cudaStream_t side = nullptr;  // look-ahead stream (tile POTRF of the next panel)
   cudaEvent_t ev_col = nullptr, ev_fact = nullptr;
 };

@@ -380,6 +380,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     for (int J = 0; J + 1 < T && J < 4096; ++J) {
       const StepMarks& m = sm_[J];
       const double kk = (double)(T - J - 1);
+      if (J < 4096) ctx->step_ms[J] = el(prev, m.gemm_end);
       if (la_mode == 1) {
         ctx->prof[2] += el(prev, m.gemm_end);  // update + fused TRSM of the next panel
         ctx->prof[0] += el(m.p0, m.p1);
@@ -400,6 +401,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     if (m_wait >= 0) ctx->prof[9] += el(m_last, m_wait);
     ctx->prof[8] += el(m_start, m_wait >= 0 ? m_wait : m_last);
     ctx->prof[7] += 1;
+    ctx->nsteps = T - 1 < 4096 ? T - 1 : 4096;
   }
   return rc;
 }
@@ -407,6 +409,12 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
 int bgp_set_profiling(bgp_ctx_t ctx, int on) {
   ctx->profile = (on != 0);
   return BGP_OK;
+}
+
+int bgp_profile_steps(bgp_ctx_t ctx, double* out, int max) {
+  const int n = ctx->nsteps < max ? ctx->nsteps : max;
+  for (int i = 0; i < n; ++i) out[i] = ctx->step_ms[i];
+  return n;
 }
 
 int bgp_profile_read(bgp_ctx_t ctx, double* out) {
@@ -614,6 +622,18 @@ int bgp_tile_potrf(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0, int6
   const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s))) return rc;
+  return read_info(ctx, s, info);
+}
+
+int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv, int64_t* info, void* stream) {
+  if (!valid_tile(tile) || !linv) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
+  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, 0, ctx->d_dinv, s))) return rc;
+  if ((rc = launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s, nullptr, true))) return rc;
   return read_info(ctx, s, info);
 }
 

@@ -309,11 +309,45 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const double* __restrict__
 // and only needs diagonals < d, so all blocks of a diagonal are independent.
 // Both products run on DMMA with fragments loaded from L2 (the tile was just
 // factored); the partial sums of a diagonal are staged in shared memory.
-constexpr int TINV_THREADS = 512;
+constexpr int TINV_THREADS = 256;
+
+// acc (32x32 block as 4x4 8x8 DMMA tiles) += A(32x32) B(32x32): A(r, k) at
+// a[k * lda + r], B(k, c) at bm[c * ldb + k] (both column-major, from L2);
+// all 64 fragments of a k range are loaded before the 128 DMMAs.
+__device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double* __restrict__ a, int64_t lda,
+                                            const double* __restrict__ bm, int64_t ldb, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+#pragma unroll
+  for (int kh = 0; kh < 2; ++kh) {  // two halves of k (16 each) to bound registers
+    double av[4][4], bv[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = kh * 16 + 4 * k + s4;
+        av[k][t] = __ldcg(a + (int64_t)kk * lda + t * 8 + q);
+        bv[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * ldb + kk);
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[k][tr], bv[k][tc]);
+  }
+}
+
+// Single-CTA inverse of a factored diagonal tile for the look-ahead stream
+// (where only one SM is free): Linv = L^{-1} by block diagonals.  Diagonal
+// d holds the blocks (j + d, j); each is
+//   Linv[j+d][j] = -Dinv_{j+d} * sum_{m=j}^{j+d-1} L[j+d][m] Linv[m][j]
+// and only needs diagonals < d, so all blocks of a diagonal are independent:
+// one warp per 32x32 block, 4x4 DMMA tiles, 64 fragment loads (L2: the tile
+// was just factored) in flight per 128 DMMAs.
 __global__ void __launch_bounds__(TINV_THREADS, 1)
     tri_inv_diag_kernel(const double* __restrict__ L, const double* __restrict__ dinv, int b,
                         double* __restrict__ Linv, int* __restrict__ done) {
-  extern __shared__ double S[];  // diagonal partial sums: block j at [(j*32 + r)*33 + c]
+  extern __shared__ double S[];  // per warp: one 32x32 partial sum, [(w*32 + r)*33 + c]
   const int nbk = b / NB;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nw = TINV_THREADS / 32;
@@ -326,45 +360,53 @@ __global__ void __launch_bounds__(TINV_THREADS, 1)
     else if (bi == bj) Linv[idx] = dinv[(int64_t)bj * NB * NB + (c % NB) * NB + (r % NB)];
   }
   __syncthreads();
+  double* Sw = S + (size_t)warp * NB * 33;
   for (int d = 1; d < nbk; ++d) {
-    const int nblocks = nbk - d;
-    // S_j = sum_m L[j+d][m] Linv[m][j]: one 8x8 output tile per warp task
-    for (int t = warp; t < nblocks * 16; t += nw) {
-      const int j = t >> 4, tr = (t >> 2) & 3, tc = t & 3, i = j + d;
-      double c0 = 0.0, c1 = 0.0;
-      for (int m = j; m < i; ++m) {
-        const double* La = L + (int64_t)(m * NB + s4) * b + i * NB + tr * 8 + q;      // A[q][k] = L[row][32m+k]
-        const double* Lb = Linv + (int64_t)(j * NB + tc * 8 + q) * b + m * NB + s4;  // B[k][q] = Linv[32m+k][col]
-        double av[8], bv[8];
+    for (int j = warp; j < nbk - d; j += nw) {
+      const int i = j + d;
+      double acc[4][4][2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          av[k] = __ldcg(La + (int64_t)(4 * k) * b);
-          bv[k] = __ldcg(Lb + 4 * k);
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+      // S = sum_m L[i][m] Linv[m][j]
+      for (int m = j; m < i; ++m)
+        block_mma32(acc, L + (int64_t)(m * NB) * b + i * NB, b, Linv + (int64_t)(j * NB) * b + m * NB, b, lane);
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) {
+          Sw[(tr * 8 + q) * 33 + tc * 8 + 2 * s4] = acc[tr][tc][0];
+          Sw[(tr * 8 + q) * 33 + tc * 8 + 2 * s4 + 1] = acc[tr][tc][1];
+          acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dmma884(c0, c1, av[k], bv[k]);
-      }
-      double* Sj = S + (size_t)(j * NB + tr * 8 + q) * 33 + tc * 8 + 2 * s4;
-      Sj[0] = c0;
-      Sj[1] = c1;
-    }
-    __syncthreads();
-    // Linv[j+d][j] = -Dinv_{j+d} S_j
-    for (int t = warp; t < nblocks * 16; t += nw) {
-      const int j = t >> 4, tr = (t >> 2) & 3, tc = t & 3, i = j + d;
-      const double* Di = dinv + (int64_t)i * NB * NB;  // column-major 32x32
-      double c0 = 0.0, c1 = 0.0;
+      __syncwarp();
+      // Linv[i][j] = -Dinv_i S   (Dinv column-major 32x32; S row-major, ld 33)
+      const double* Di = dinv + (int64_t)i * NB * NB;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const double a = Di[(4 * k + s4) * NB + tr * 8 + q];
-        const double bb = S[(size_t)(j * NB + 4 * k + s4) * 33 + tc * 8 + q];
-        dmma884(c0, c1, a, bb);
+        double av[4], bv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          av[t] = Di[(4 * k + s4) * NB + t * 8 + q];
+          bv[t] = Sw[(4 * k + s4) * 33 + t * 8 + q];
+        }
+#pragma unroll
+        for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+          for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[tr], bv[tc]);
       }
-      const int row = i * NB + tr * 8 + q, col = j * NB + tc * 8 + 2 * s4;
-      Linv[(int64_t)col * b + row] = -c0;
-      Linv[(int64_t)(col + 1) * b + row] = -c1;
+      __syncwarp();
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) {
+          const int row = i * NB + tr * 8 + q, col = j * NB + tc * 8 + 2 * s4;
+          Linv[(int64_t)col * b + row] = -acc[tr][tc][0];
+          Linv[(int64_t)(col + 1) * b + row] = -acc[tr][tc][1];
+        }
     }
-    __syncthreads();
+    __syncthreads();  // diagonal d complete before d + 1 reads it
   }
   if (done) {  // publish: the fused panel TRSM of the trailing update waits for this
     __threadfence();
@@ -504,8 +546,8 @@ int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv,
 int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
                    int* done, bool one_cta) {
   if (one_cta) {
-    const size_t smem = (size_t)(b / NB - 1) * NB * 33 * sizeof(double);
-    tri_inv_diag_kernel<<<1, TINV_THREADS, smem > 0 ? smem : 8, s>>>(Ltile, dinv, b, Linv, done);
+    const size_t smem = (size_t)(TINV_THREADS / 32) * NB * 33 * sizeof(double);
+    tri_inv_diag_kernel<<<1, TINV_THREADS, smem, s>>>(Ltile, dinv, b, Linv, done);
     ctx->launches++;
     return check_launch(ctx, "tri_inv_diag");
   }

@@ -65,3 +65,22 @@ def test_lookahead_late_failure(cluster_factory, tile):
     C2 = distla.distribute(cl, "C2", A2, "triangular", lay)
     L2, _ = distla.distributed_cholesky(cl, C2, "L2")
     assert relerr(distla.collect(cl, L2), np.linalg.cholesky(A2)) <= 1e-12
+
+
+@pytest.mark.parametrize("tile", [128, 256, 384, 512])
+def test_tile_inverse(cluster_factory, tile):
+    """The one-CTA block-diagonal inverse the fused panel TRSM uses."""
+    import ctypes
+    import torch
+    cl = cluster_factory(tile=tile)
+    A = spd_matrix(tile, seed=tile)
+    t = torch.from_numpy(np.tril(A).T.copy()).to(cl.device)  # column-major lower tile
+    linv = torch.empty_like(t)
+    info = ctypes.c_int64()
+    rc = cl.lib.bgp_tile_potrf_inv(cl._ctx, ctypes.c_void_p(t.data_ptr()), tile,
+                                   ctypes.c_void_p(linv.data_ptr()), ctypes.byref(info), cl.stream)
+    assert rc == 0 and info.value == 0
+    L = np.linalg.cholesky(A)
+    got = linv.cpu().numpy().T  # column-major -> row-major
+    assert relerr(got, np.linalg.inv(L)) <= 1e-12
+    assert np.all(np.triu(got, 1) == 0.0)

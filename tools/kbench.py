@@ -59,6 +59,15 @@ def main():
     us = time_it(potrf) - copy_us
     print(json.dumps({"kernel": "tile_potrf (incl. status sync)", "b": b, "us": round(us, 1),
                       "gflops": round(b ** 3 / 3 / us / 1e3, 1)}))
+    linv = torch.empty_like(tile0)
+
+    def potrf_inv():
+        work.copy_(tile0)
+        lib.bgp_tile_potrf_inv(ctx, p(work), b, p(linv), ctypes.byref(info), s)
+
+    us2 = time_it(potrf_inv) - copy_us
+    print(json.dumps({"kernel": "tile_potrf + one-CTA inverse (incl. status sync)", "b": b, "us": round(us2, 1),
+                      "inverse_us": round(us2 - us, 1)}))
     L = work.clone()
     for k in (1, 32, 128, 262):
         panel = torch.from_numpy(rng.standard_normal((k, b, b))).to(dev)
