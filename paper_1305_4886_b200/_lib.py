@@ -11,7 +11,8 @@ import os
 from .errors import BackendUnavailable
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbgp.so")
+# BGP_LIB_PATH (diagnostics): load an alternative build, e.g. a probe variant
+LIB_PATH = os.environ.get("BGP_LIB_PATH") or os.path.join(_HERE, "libbgp.so")
 
 BGP_OK = 0
 BGP_E_CUDA = -1

@@ -31,7 +31,14 @@
 
 #include <stdio.h>
 
+// Compiled twice: here with the BK = 16 configuration (namespace bgp::bk16)
+// and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks per tile.
+#ifndef BGP_GEMM_NS
+#define BGP_GEMM_NS bk16
+#endif
+
 namespace bgp {
+namespace BGP_GEMM_NS {
 
 // Tile configuration.  One CTA per SM, three warpgroups:
 //   WG0  producers: warp 0 feeds consumer group 0's ring, warp 1 group 1's
@@ -41,7 +48,11 @@ namespace bgp {
 // The two consumer groups take alternate blocks of the CTA's static schedule
 // and run concurrently, so one group's epilogue overlaps the other group's
 // main loop and the DMMA pipe never drains between blocks.
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+#ifdef BGP_GEMM_BK32  // 2 stages of BK = 32, epilogue in 16-row rounds
+constexpr int BM = 128, BN = 64, BK = 32, STAGES = 2, EPI_ROWS = 16;
+#else
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 32;
+#endif
 constexpr int GROUPS = 2;
 constexpr int WARPS_M = 2, WARPS_N = 2;       // per consumer group
 constexpr int GROUP_WARPS = WARPS_M * WARPS_N;
@@ -53,8 +64,11 @@ constexpr int STAGE_A_BYTES = BM * BK * 8;     // 16 KB: 8 boxes
 constexpr int STAGE_B_BYTES = BN * BK * 8;     // 8 KB: 4 boxes
 constexpr int STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr int WBOX_BYTES = 16 * WN * 8;        // 4 KB: epilogue box of 16 rows x 32 cols
-constexpr int WSTAGE_BYTES = 2 * WBOX_BYTES;   // 8 KB: a warp's epilogue slice (half its tile)
-constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;  // 32 KB per group
+constexpr int EPI_BOXES = EPI_ROWS / 16;       // boxes per epilogue round
+constexpr int EPI_ROUNDS = 64 / EPI_ROWS;      // rounds per 64-row warp tile
+constexpr int WSTAGE_BYTES = EPI_BOXES * WBOX_BYTES;  // a warp's epilogue slice (one round)
+constexpr int HALVES = BK / 4;                 // k4 half-steps per stage
+constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
@@ -411,22 +425,23 @@ __device__ __forceinline__ void sts64(uint32_t base, double v) {
   asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(base), "n"(OFF), "d"(v) : "memory");
 }
 
-// Stage rows ii = 0..3 (of 8-row blocks i = 4r + ii) of the warp's 64x32
-// accumulator tile into its 8 KB epilogue slice: two 16x32 boxes, 128B
-// swizzled like the operands (line = column n).  cb[p][e] are the lane's
-// addresses of (row-pair p, column parity e) in box 0, column block j = 0.
-// NEG stages -acc (integer sign flip, no FP64 instruction); MASK zeroes the
-// strict upper triangle of a diagonal tile (m < n).
+// Stage the 8-row blocks i = R*NII + ii (ii < NII) of the warp's 64x32
+// accumulator tile into its epilogue slice: NII/2 16x32 boxes, 128B swizzled
+// like the operands (line = column n).  cb[p][e] are the lane's addresses of
+// (row-pair p, column parity e) in box 0, column block j = 0.  NEG stages
+// -acc (integer sign flip, no FP64 instruction); MASK zeroes the strict upper
+// triangle of a diagonal tile (m < n).
 template <int R, bool NEG, bool MASK>
 __device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const uint32_t (&cb)[2][2], int m0,
                                            int n0) {
+  constexpr int NII = EPI_ROWS / 8;
 #pragma unroll
-  for (int ii = 0; ii < MI / 2; ++ii) {
+  for (int ii = 0; ii < NII; ++ii) {
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        double v = acc[R * (MI / 2) + ii][j][e];
+        double v = acc[R * NII + ii][j][e];
         if (NEG) v = __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull);
         if (MASK && m0 + ii * 8 < n0 + j * 8 + e) v = 0.0;
         const uint32_t a = cb[ii & 1][e];
@@ -442,6 +457,33 @@ __device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const
         }
       }
     }
+  }
+}
+
+// epilogue round R: stage (NEG / MASK chosen per block) then TMA the boxes
+template <int R>
+__device__ __forceinline__ void stage_round(const double (&acc)[MI][NJ][2], const uint32_t (&cb)[2][2], int m0,
+                                            int n0, bool store, bool lower) {
+  if (store) {
+    if (lower) stage_rows<R, false, true>(acc, cb, m0, n0);
+    else stage_rows<R, false, false>(acc, cb, m0, n0);
+  } else {
+    if (lower) stage_rows<R, true, true>(acc, cb, m0, n0);
+    else stage_rows<R, true, false>(acc, cb, m0, n0);
+  }
+}
+
+// half-steps H .. HALVES-2 of a stage: load the fragments of H+1, issue the
+// DMMAs of H (compile-time recursion so every offset is an immediate)
+template <int H>
+__device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ][2], const uint32_t (&offA)[2][2],
+                                             const uint32_t (&offB)[2][2], uint32_t sb) {
+  if constexpr (H + 1 < HALVES) {
+    constexpr int N = H + 1;
+    load_frag<(N >> 1)>(f[N & 1], offA[0][N & 1] + sb, offA[1][N & 1] + sb, offB[0][N & 1] + sb,
+                        offB[1][N & 1] + sb);
+    mma_frag(acc, f[H & 1]);
+    stage_halves<H + 1>(f, acc, offA, offB, sb);
   }
 }
 
@@ -505,11 +547,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][0] = clock64();
 #endif
-    Frag x, y;
+    Frag f[2];
     uint32_t sb = (uint32_t)stage * STAGE_BYTES;
-#define BGP_LOAD(F, H) load_frag<((H) >> 1)>(F, offA[0][(H) & 1] + sb, offA[1][(H) & 1] + sb, \
-                                             offB[0][(H) & 1] + sb, offB[1][(H) & 1] + sb)
-    BGP_LOAD(x, 0);
+    load_frag<0>(f[0], offA[0][0] + sb, offA[1][0] + sb, offB[0][0] + sb, offB[1][0] + sb);
     for (int kc = 0; kc + 1 < nk; ++kc) {
       const int cur = stage;
       if (stagger_arrive && kc == (nk >> 1)) {
@@ -517,31 +557,20 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         if (lane == 0) mbar_arrive(stagger);
         stagger_arrive = false;
       }
-      BGP_LOAD(y, 1);
-      mma_frag(acc, x);
-      BGP_LOAD(x, 2);
-      mma_frag(acc, y);
-      BGP_LOAD(y, 3);
-      mma_frag(acc, x);
+      stage_halves<0>(f, acc, offA, offB, sb);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
       }
       sb = (uint32_t)stage * STAGE_BYTES;
       mbar_wait(&gs.full[stage], phase);
-      BGP_LOAD(x, 0);
-      mma_frag(acc, y);
+      load_frag<0>(f[0], offA[0][0] + sb, offA[1][0] + sb, offB[0][0] + sb, offB[1][0] + sb);
+      mma_frag(acc, f[(HALVES - 1) & 1]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[cur]);
     }
-    BGP_LOAD(y, 1);
-    mma_frag(acc, x);
-    BGP_LOAD(x, 2);
-    mma_frag(acc, y);
-    BGP_LOAD(y, 3);
-    mma_frag(acc, x);
-    mma_frag(acc, y);
-#undef BGP_LOAD
+    stage_halves<0>(f, acc, offA, offB, sb);
+    mma_frag(acc, f[(HALVES - 1) & 1]);
     __syncwarp();
     if (lane == 0) mbar_arrive(&gs.empty[stage]);
     if (++stage == STAGES) {
@@ -572,34 +601,23 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     continue;
 #endif
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (lane == 0 && (store_pending || r == 1)) tma_store_wait_read0();  // slice free again
+    for (int r = 0; r < EPI_ROUNDS; ++r) {
+      if (lane == 0 && (store_pending || r > 0)) tma_store_wait_read0();  // slice free again
       __syncwarp();
       // row m = m0 + ii*8 of the round, column n = n0 + j*8 + e (tile coordinates)
-      const int m0 = it.mrow0 + wm * WM + r * (WM / 2) + q, n0 = it.nrow0 + wn * WN + 2 * s4;
-      if (it.store) {
-        if (it.lower) {
-          if (r == 0) stage_rows<0, false, true>(acc, cbase, m0, n0);
-          else stage_rows<1, false, true>(acc, cbase, m0, n0);
-        } else {
-          if (r == 0) stage_rows<0, false, false>(acc, cbase, m0, n0);
-          else stage_rows<1, false, false>(acc, cbase, m0, n0);
-        }
-      } else {
-        if (it.lower) {
-          if (r == 0) stage_rows<0, true, true>(acc, cbase, m0, n0);
-          else stage_rows<1, true, true>(acc, cbase, m0, n0);
-        } else {
-          if (r == 0) stage_rows<0, true, false>(acc, cbase, m0, n0);
-          else stage_rows<1, true, false>(acc, cbase, m0, n0);
-        }
+      const int m0 = it.mrow0 + wm * WM + r * EPI_ROWS + q, n0 = it.nrow0 + wn * WN + 2 * s4;
+      switch (r) {
+        case 0: stage_round<0>(acc, cbase, m0, n0, it.store, it.lower); break;
+        case 1: stage_round<1>(acc, cbase, m0, n0, it.store, it.lower); break;
+        case 2: stage_round<2>(acc, cbase, m0, n0, it.store, it.lower); break;
+        default: stage_round<3>(acc, cbase, m0, n0, it.store, it.lower); break;
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        const int r0 = it.mrow0 + wm * WM + r * (WM / 2), c0 = it.nrow0 + wn * WN;
+        const int r0 = it.mrow0 + wm * WM + r * EPI_ROWS, c0 = it.nrow0 + wn * WN;
 #pragma unroll
-        for (int b2 = 0; b2 < 2; ++b2) {
+        for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
           if (it.store)
             tma_store_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
           else
@@ -668,7 +686,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // One-time function setup.  It also forces the module to load: with CUDA's
 // lazy loading, the first launch of a kernel while a spin-waiting kernel runs
 // on another stream (the look-ahead POTRF) could otherwise stall behind it.
-void gemm_prepare() {
+void prepare() {
   static int occupancy = -1;
   if (occupancy < 0) {
     cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -678,8 +696,8 @@ void gemm_prepare() {
   }
 }
 
-int launch_gemm(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase, int64_t nA,
-                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
+int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase, int64_t nA,
+           const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
   if (p_in.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
   GemmProblem p = p_in;
   const int64_t tasks = gemm_num_tasks(p);
@@ -696,7 +714,7 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* 
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mL, Linv ? Linv : Bbase, p.b, Linv ? 1 : nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
-  gemm_prepare();
+  prepare();
   const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
   const int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
@@ -705,10 +723,32 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* 
   return check_launch(ctx, "gemm_dmma");
 }
 
+}  // namespace BGP_GEMM_NS
+
+#ifndef BGP_GEMM_SECONDARY
+namespace bk32 {
+void prepare();
+int launch(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA, const double* Bbase,
+           int64_t nB, int64_t nC, cudaStream_t s, const double* Linv);
+}  // namespace bk32
+
+void gemm_prepare() {
+  bk16::prepare();
+  bk32::prepare();
+}
+
+// 512 tiles: BK = 32 stages (half the barrier and TMA operations per DMMA);
+// smaller tiles keep BK = 16 (measured: C4 at b = 512 +0.9 %, b = 256 -1.7 %)
+int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
+                const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
+  if (p.b >= 512) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
+  return bk16::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
+}
+#endif
 }  // namespace bgp
 
-#ifdef BGP_EXP_TRACE
+#if defined(BGP_EXP_TRACE) && !defined(BGP_GEMM_SECONDARY)
 extern "C" int bgp_probe_trace(void* host_out) {
-  return (int)cudaMemcpyFromSymbol(host_out, bgp::g_trace, sizeof(bgp::g_trace));
+  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_trace, sizeof(bgp::bk16::g_trace));
 }
 #endif

@@ -10,13 +10,14 @@ if [ "$1" = "build" ]; then
       base) F="";; NO_TMA) F="-DBGP_EXP_NO_TMA";; NO_EPI) F="-DBGP_EXP_NO_EPI";;
       NO_TMA_NO_EPI) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       TRACE) F="-DBGP_EXP_TRACE";;
+      BK32) F="-DBGP_GEMM_BK32";;
       NO_BAR_TRACE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR -DBGP_EXP_TRACE";;
       NO_BAR) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR";;
     esac
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $F $EXTRA \
       -c paper_1305_4886_b200/csrc/gemm.cu -o $D/gemm_$v.o
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/libbgp_$v.so build/capi.o build/cov.o \
-      build/potrf.o $D/gemm_$v.o build/solve.o build/rng.o build/trsv.o
+      build/potrf.o $D/gemm_$v.o build/solve.o build/rng.o build/trsv.o build/gemm_bk32.o
   done
 else
   mkdir -p gpurun_out/probe
