@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 SRC_DIR := paper_1305_4886_b200/csrc
 SRCS := $(SRC_DIR)/capi.cu $(SRC_DIR)/cov.cu $(SRC_DIR)/potrf.cu $(SRC_DIR)/gemm.cu $(SRC_DIR)/solve.cu $(SRC_DIR)/rng.cu $(SRC_DIR)/trsv.cu $(SRC_DIR)/gemm_bk32.cu
-HDRS := $(SRC_DIR)/bgp_common.cuh $(SRC_DIR)/bgp_internal.h include/bgp.h
+HDRS := $(SRC_DIR)/bgp_common.cuh $(SRC_DIR)/bgp_internal.h $(SRC_DIR)/panel_device.cuh include/bgp.h
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB := paper_1305_4886_b200/libbgp.so
 

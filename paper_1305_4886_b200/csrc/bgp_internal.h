@@ -51,8 +51,6 @@ struct Ctx {
   double prof[BGP_PROFILE_SLOTS] = {};
   double step_ms[4096] = {};  // per-step update-launch time of the last profiled factorization
   int nsteps = 0;
-  cudaStream_t side = nullptr;  // look-ahead stream (tile POTRF of the next panel)
-  cudaEvent_t ev_col = nullptr, ev_fact = nullptr;
 };
 
 int set_err(Ctx* ctx, const char* what, cudaError_t e);
@@ -80,6 +78,8 @@ int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_
 // loading must not happen while a look-ahead kernel spin-waits)
 void gemm_prepare();
 void potrf_prepare();
+size_t potrf_smem_bytes(int b);
+size_t tri_inv_smem_bytes();
 
 // tile kernels
 // info value reserved for a look-ahead wait that never completed (a bug, not data)
@@ -122,9 +122,18 @@ struct GemmProblem {
   int* col_gate;
   int trsm_next;
   int tile_need;
-  const int* linv_flag;
+  int* linv_flag;
   int linv_need;
   int trsm_tail;       // update blocks queued after the fused TRSM tasks (tail filler)
+  // look-ahead inside the launch: the last CTA first factors tile potrf_tile
+  // (panel J+1's diagonal, once col_gate[0] reaches diag_need) into dinv, and
+  // with trsm_next its inverse into linv (published through linv_flag), then
+  // joins the queue
+  double* potrf_tile;
+  int64_t potrf_row0;
+  double* dinv;
+  double* linv;
+  int diag_need;
 };
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv = nullptr);

@@ -169,9 +169,6 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_sync) cudaFree(ctx->d_sync);
   if (ctx->d_gate) cudaFree(ctx->d_gate);
   if (ctx->d_linv) cudaFree(ctx->d_linv);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
-  if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
-  if (ctx->ev_fact) cudaEventDestroy(ctx->ev_fact);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
   delete[] ctx->events;
   delete ctx;
@@ -200,19 +197,18 @@ static int diag_tile_blocks(int b) {
   return c;
 }
 
-// Right-looking tile Cholesky with a one-panel look-ahead, two launches per
-// step.  The step-J trailing update is one persistent DMMA launch on all SMs
-// but one.  Its task queue holds the update blocks (tile column J+1 first)
-// followed by the in-place TRSM of panel J+1.  Warps that reduce into a tile
-// of column J+1 bump that tile's counter once their bulk reductions retired.
-// On the side stream, on the spare SM, the tile POTRF of J+1 waits for the
-// diagonal tile's counter, factors it, and tri_inv publishes its inverse;
-// the update's TRSM tasks wait for their tile's counter and that flag.  So the
-// latency-bound POTRF and the panel TRSM both run under the trailing update,
-// and the TRSM fills the update's tail instead of adding a launch.  Waits are
-// one-way (update -> POTRF -> TRSM tasks, never back), bounded, and reported
-// as errors if they ever time out.  The only host synchronization is the
-// final status read.
+// Right-looking tile Cholesky with a one-panel look-ahead, one launch per
+// step.  The step-J trailing update is one persistent DMMA launch whose task
+// queue holds the update blocks (tile column J+1 first), the in-place TRSM of
+// panel J+1, and a tail of update blocks.  Warps that reduce into a tile of
+// column J+1 bump that tile's counter once their bulk reductions retired.
+// The launch's last CTA first waits for the diagonal tile's counter, factors
+// tile (J+1, J+1) and inverts it on its ring memory, publishes the inverse,
+// and then joins the queue; the TRSM tasks wait for their tile's counter and
+// the inverse.  So the latency-bound POTRF and the panel TRSM both run under
+// the trailing update.  Waits are one-way (update blocks -> POTRF -> TRSM
+// tasks, never back), bounded, and reported as errors if they time out.  The
+// only host synchronization is the final status read.
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
   if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -228,12 +224,6 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   const int stride = (T + 4 + 1) & ~1;
   if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
-  if (!ctx->side) {
-    cudaError_t e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_col, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fact, cudaEventDisableTiming);
-    if (e != cudaSuccess) return set_err(ctx, "look-ahead stream", e);
-  }
   {
     cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
     if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
@@ -245,18 +235,15 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   const int nblk = (b / 128) * (b / 64);                 // 128x64 blocks per tile (gemm.cu)
   const int diag_need = diag_tile_blocks(b) * 4;         // 4 warps per block (gemm.cu GROUP_WARPS)
   const int tile_need = nblk * 4;
-  // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead; 0 sequential on
-  // all SMs; 2 sequential with the trailing update on all SMs but one.  The
-  // look-ahead POTRF waits on a kernel running concurrently, so it is off
-  // when kernels are serialised (CUDA_LAUNCH_BLOCKING=1, or Nsight Compute,
-  // which replays kernels one at a time).
+  // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead inside the update
+  // launch; 0 sequential launches on all SMs; 2 sequential with the update on
+  // all SMs but one.  All look-ahead waits are inside one launch, so the
+  // schedule also holds when kernels are serialised (Nsight Compute).
   static const int la_mode = [] {
     if (const char* e = getenv("BGP_LOOKAHEAD")) return atoi(e);
-    const char* blocking = getenv("CUDA_LAUNCH_BLOCKING");
-    if ((blocking && atoi(blocking) != 0) || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE")) return 0;
     return 1;
   }();
-  // profiling: main-stream marks, side-stream POTRF start/end pairs
+  // profiling: marks on the caller's stream around every launch
   const int nev = 3 * T + 8;
   if (ctx->profile && ctx->events_cap < nev) {
     for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
@@ -279,8 +266,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
   // tri_inv of K (needed when panel K has tiles below the diagonal)
   auto inverse = [&](int K, cudaStream_t st, int* done) -> int {
     if (K + 1 >= T) return BGP_OK;
-    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st, done,
-                          st == ctx->side);
+    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st, done, true);
   };
   // standalone panel solve of K on the caller's stream
   auto panel_solve = [&](int K) -> int {
@@ -324,22 +310,19 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     p.check_info = true;
     p.queue = gate + stride - 2;
     if (la_mode == 1) {
-      // POTRF(K) + inverse on the side stream once the previous launch (which
-      // read the shared inverse buffers) is done; they run on the spare SM
-      cudaEventRecord(ctx->ev_col, s);
-      cudaStreamWaitEvent(ctx->side, ctx->ev_col, 0);
-      sm.p0 = mark(ctx->side);
-      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, ctx->side, gate, diag_need)))
-        return rc;
-      if ((rc = inverse(K, ctx->side, gate + T))) return rc;
-      sm.p1 = mark(ctx->side);
-      p.grid_limit = ctx->num_sms - 1;
+      // POTRF(K) (+ inverse) by the launch's last CTA, the TRSM of panel K as
+      // gated tasks of the same launch
       p.col_gate = gate;
       p.trsm_next = (K + 1 < T);
       p.tile_need = tile_need;
       p.linv_flag = gate + T;
       p.linv_need = nbk;
       p.trsm_tail = 12 * ctx->num_sms;  // ~6 update blocks per consumer group
+      p.potrf_tile = dkk;
+      p.potrf_row0 = (int64_t)K * b;
+      p.dinv = ctx->d_dinv;
+      p.linv = ctx->d_linv;
+      p.diag_need = diag_need;
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
       sm.gemm_end = mark(s);
     } else {
@@ -359,12 +342,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     if (J < 4096) sm_[J] = sm;
     m_last = sm.gemm_end;
   }
-  int m_wait = -1;
-  if (la_mode == 1) {  // the last POTRF ran on the side stream
-    cudaEventRecord(ctx->ev_fact, ctx->side);
-    cudaStreamWaitEvent(s, ctx->ev_fact, 0);
-    m_wait = mark(s);
-  }
+  const int m_wait = -1;
   rc = read_info(ctx, s, info);
   if (rc == BGP_OK && info && (unsigned long long)*info >= BGP_INFO_DATAFLOW_TIMEOUT) {
     ctx->err = "look-ahead wait timed out (internal dependency error)";
@@ -382,8 +360,7 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
       const double kk = (double)(T - J - 1);
       if (J < 4096) ctx->step_ms[J] = el(prev, m.gemm_end);
       if (la_mode == 1) {
-        ctx->prof[2] += el(prev, m.gemm_end);  // update + fused TRSM of the next panel
-        ctx->prof[0] += el(m.p0, m.p1);
+        ctx->prof[2] += el(prev, m.gemm_end);  // update + POTRF / inverse / TRSM of the next panel
         ctx->prof[4] += (double)b * b * b * (kk * kk + (kk - 1.0));
         prev = m.gemm_end;
       } else {

@@ -28,6 +28,7 @@
 // 16 lanes of each half-warp hit 16 distinct 8-byte slots.
 #include "bgp_common.cuh"
 #include "bgp_internal.h"
+#include "panel_device.cuh"
 
 #include <stdio.h>
 
@@ -652,8 +653,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmC,
-                     const GemmProblem p, const unsigned long long* __restrict__ info) {
+                     const GemmProblem p, unsigned long long* __restrict__ info) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ int s_go;
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
   if (info && *(volatile const unsigned long long*)info != 0ull) return;  // factorization failed
 
@@ -671,13 +673,32 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  // look-ahead CTA: factor (and invert) the next panel's diagonal tile first
+  const bool lookahead_cta = p.potrf_tile != nullptr && blockIdx.x == gridDim.x - 1;
 
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+    if (lookahead_cta) named_bar_sync(1, THREADS);  // wait for the panel work below
     if (warp < GROUPS && lane == 0)
       producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmC, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+    if (lookahead_cta) {
+      // the 256 consumer threads run the tile POTRF (and inverse) on the ring
+      // memory once the update blocks of the diagonal tile retired; other
+      // CTAs' TRSM tasks wait for the published inverse
+      const int ctid = threadIdx.x - 128;
+      double* psm = reinterpret_cast<double*>(smem);
+      if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
+      named_bar_sync(2, 256);
+      if (s_go && tile_potrf_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info, psm, ctid, 2) && p.trsm_next) {
+        tri_inv_diag_device(p.potrf_tile, p.dinv, p.b, p.linv, psm, ctid, 2);
+        __threadfence();
+        named_bar_sync(2, 256);
+        if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);
+      }
+      named_bar_sync(1, THREADS);  // release this CTA's producers
+    }
     const int g = wg - 1;
     consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem));
   }
@@ -716,7 +737,16 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
   prepare();
   const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
-  const int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
+  int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
+  if (p.potrf_tile && grid < 2) grid = 2;  // the look-ahead CTA must not be the only one
+  if (p.potrf_tile) {
+    static bool attr = false;
+    if (!attr) {  // the look-ahead CTA's device POTRF / inverse must fit the ring memory
+      if (potrf_smem_bytes(p.b) > (size_t)(GROUPS * GROUP_BYTES) || tri_inv_smem_bytes() > (size_t)(GROUPS * GROUP_BYTES))
+        return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
+      attr = true;
+    }
+  }
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
                                                                   p.check_info ? ctx->d_info : nullptr);
   ctx->launches++;

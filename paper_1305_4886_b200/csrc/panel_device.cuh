@@ -1,0 +1,318 @@
+// Device code of the tile POTRF and the one-CTA tile inverse, shared by the
+// standalone kernels (potrf.cu) and the look-ahead CTA of the trailing-update
+// launch (gemm.cu).  See potrf.cu for the algorithms.
+#pragma once
+
+#include "bgp_common.cuh"
+#include "bgp_internal.h"
+
+namespace bgp {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NB = 32;        // sub-panel width
+constexpr int PLD = 36;       // smem leading dimension of the panel copy (conflict-free DMMA frags)
+constexpr int POTRF_THREADS = 256;
+
+// inverse of a lower-triangular 32x32 block held in smem D (ld 33);
+// lane = column of the inverse.  rdiag (smem, optional) holds 1/D[i][i]; the
+// dot products use four partial sums to shorten the dependent FMA chain.
+// Writes Dinv_s (ld 33) and optionally global (column-major 32x32).
+__device__ __forceinline__ void warp_trinv32(const double* D, const double* rdiag, double* Dinv_s, double* gout,
+                                             int lane) {
+  double x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      const double t = D[i * 33 + k] * x[k];
+      if ((k & 3) == 0) s0 += t;
+      else if ((k & 3) == 1) s1 += t;
+      else if ((k & 3) == 2) s2 += t;
+      else s3 += t;
+    }
+    const double r = rdiag ? rdiag[i] : 1.0 / D[i * 33 + i];
+    x[i] = (i == lane) ? r : ((i > lane) ? -((s0 + s1) + (s2 + s3)) * r : 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    Dinv_s[i * 33 + lane] = x[i];
+    if (gout) gout[lane * NB + i] = x[i];
+  }
+}
+
+// Factor the 32x32 diagonal block at (c0, c0) of the tile in global memory
+// (warp-wide; lane = row, column j exchanged through smem `col`), store L in
+// A and D, 1/L_jj in rdiag.  Returns the failure bitmask (warp-uniform).
+__device__ __forceinline__ unsigned warp_potrf32(double* A, int b, int c0, double* D, double* rdiag,
+                                                 double* col, int lane) {
+  double a[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) a[j] = (j <= lane) ? A[(int64_t)(c0 + j) * b + c0 + lane] : 0.0;
+  unsigned failmask = 0u;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (lane == j) col[j] = a[j];
+    __syncwarp();
+    const double piv = col[j];
+    failmask |= (piv > 0.0) ? 0u : (1u << j);
+    const double rinv = rsqrt(piv > 0.0 ? piv : 1.0);
+    const double ljj = (piv > 0.0 ? piv : 1.0) * rinv;
+    if (lane == 0) rdiag[j] = rinv;
+    a[j] = (lane == j) ? ljj : ((lane > j) ? a[j] * rinv : 0.0);
+    __syncwarp();
+    col[lane] = a[j];  // column j of L (rows < j hold 0)
+    __syncwarp();
+#pragma unroll
+    for (int c = j + 1; c < NB; ++c)
+      if (lane >= c) a[c] = fma(-a[j], col[c], a[c]);
+    __syncwarp();
+  }
+  if (!failmask) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      D[lane * 33 + j] = (j <= lane) ? a[j] : 0.0;
+      if (j <= lane) A[(int64_t)(c0 + j) * b + c0 + lane] = a[j];
+    }
+  }
+  __syncwarp();
+  return failmask;
+}
+
+// In-tile trailing update A[i][j] -= sum_k P[i][k] P[j][k] on 8x8 DMMA blocks
+// blk in [first, last) of the lower triangle of the `rest` x `rest` trailing
+// part (row-major block order), handed out round-robin over `nwarps` warps
+// starting at `wid`, four blocks per iteration so the C loads overlap.
+__device__ __forceinline__ void tile_trailing(double* A, int b, int base_rc, const double* P, int first,
+                                              int last, int wid, int nwarps, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+  constexpr int U = 4;
+  for (int base = first + wid * U; base < last; base += nwarps * U) {
+    int ibs[U], jbs[U];
+    double cv[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int blk = base + u;
+      int ib = 0, jb = 0;
+      if (blk < last) {
+        ib = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+        while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+        while (ib * (ib + 1) / 2 > blk) --ib;
+        jb = blk - ib * (ib + 1) / 2;
+      }
+      ibs[u] = ib;
+      jbs[u] = jb;
+      const int64_t gr = base_rc + ib * 8 + q;
+      const int64_t gc = base_rc + jb * 8 + 2 * s4;
+      cv[u][0] = (blk < last) ? A[gc * b + gr] : 0.0;
+      cv[u][1] = (blk < last) ? A[(gc + 1) * b + gr] : 0.0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < NB / 4; ++kk) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double av = -P[(ibs[u] * 8 + q) * PLD + kk * 4 + s4];
+        const double bv = P[(jbs[u] * 8 + q) * PLD + kk * 4 + s4];
+        dmma884(cv[u][0], cv[u][1], av, bv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + u >= last) continue;
+      const int64_t gr = base_rc + ibs[u] * 8 + q;
+      const int64_t gc = base_rc + jbs[u] * 8 + 2 * s4;
+      if (ibs[u] != jbs[u] || gr >= gc) A[gc * b + gr] = cv[u][0];
+      if (ibs[u] != jbs[u] || gr >= gc + 1) A[(gc + 1) * b + gr] = cv[u][1];
+    }
+  }
+}
+
+// Right-looking blocked factorization of one b x b tile with 32-wide
+// sub-panels and a one-block look-ahead inside the tile: while warps 1..7
+// apply sub-panel k's trailing update, warp 0 updates, factors and inverts
+// diagonal block k+1, so the serial 32x32 work overlaps the DMMA update.
+// Run by 256 threads (tid 0..255) that synchronise on named barrier `bar`;
+// `sm` is potrf_smem_bytes(b) of shared memory.  Returns false on a
+// non-positive pivot (recorded in *info).  Used by tile_potrf_kernel and,
+// for the look-ahead, by one CTA of the trailing-update launch.
+static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
+                                  unsigned long long* __restrict__ info, double* sm, int tid, int bar) {
+  double* D = sm;                // 32 x 33
+  double* Dinv_s = D + NB * 33;  // 32 x 33
+  double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
+  double* rdiag = P + (b - NB) * PLD;
+  double* col = rdiag + NB;
+  int* s_fail = reinterpret_cast<int*>(col + NB);
+  const int lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) *s_fail = 0;
+  named_bar_sync(bar, POTRF_THREADS);
+  const int nbk = b / NB;
+  // prologue: factor + invert diagonal block 0
+  if (warp == 0) {
+    const unsigned fm = warp_potrf32(A, b, 0, D, rdiag, col, lane);
+    if (fm) {
+      if (lane == 0) {
+        if (info) set_info(info, row0 + __ffs(fm));
+        *s_fail = 1;
+      }
+    } else {
+      warp_trinv32(D, rdiag, Dinv_s, dinv, lane);
+    }
+  }
+  named_bar_sync(bar, POTRF_THREADS);
+  if (*s_fail) return false;
+  for (int kb = 0; kb + 1 < nbk; ++kb) {
+    const int c0 = kb * NB;
+    const int rest = b - c0 - NB;
+    // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy);
+    // Dinv is lower triangular with explicit zeros, so every dot is 32 long
+    for (int r = tid; r < rest; r += POTRF_THREADS) {
+      const int64_t gi = c0 + NB + r;
+      double av[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) av[k] = A[(int64_t)(c0 + k) * b + gi];
+#pragma unroll 2
+      for (int j = 0; j < NB; ++j) {
+        const double* dj = Dinv_s + j * 33;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; k += 2) {
+          s0 = fma(av[k], dj[k], s0);
+          s1 = fma(av[k + 1], dj[k + 1], s1);
+        }
+        const double x = s0 + s1;
+        A[(int64_t)(c0 + j) * b + gi] = x;
+        P[r * PLD + j] = x;
+      }
+    }
+    named_bar_sync(bar, POTRF_THREADS);
+    // (B) trailing update; the first 10 blocks are diagonal block k+1
+    const int nb8 = rest / 8;
+    const int nblk = nb8 * (nb8 + 1) / 2;
+    const int base_rc = c0 + NB;
+    if (warp == 0) {
+      tile_trailing(A, b, base_rc, P, 0, 10, 0, 1, lane);
+      __syncwarp();
+      __threadfence_block();
+      const unsigned fm = warp_potrf32(A, b, base_rc, D, rdiag, col, lane);
+      if (fm) {
+        if (lane == 0) {
+          if (info) set_info(info, row0 + base_rc + __ffs(fm));
+          *s_fail = 1;
+        }
+      } else {
+        warp_trinv32(D, rdiag, Dinv_s, dinv ? dinv + (int64_t)(kb + 1) * NB * NB : nullptr, lane);
+      }
+    } else {
+      tile_trailing(A, b, base_rc, P, 10, nblk, warp - 1, POTRF_THREADS / 32 - 1, lane);
+    }
+    named_bar_sync(bar, POTRF_THREADS);
+    if (*s_fail) return false;
+  }
+  return true;
+}
+
+constexpr int TINV_THREADS = 256;
+
+// acc (32x32 block as 4x4 8x8 DMMA tiles) += A(32x32) B(32x32): A(r, k) at
+// a[k * lda + r], B(k, c) at bm[c * ldb + k] (both column-major, from L2);
+// all 64 fragments of a k range are loaded before the 128 DMMAs.
+__device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double* __restrict__ a, int64_t lda,
+                                            const double* __restrict__ bm, int64_t ldb, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+#pragma unroll
+  for (int kh = 0; kh < 2; ++kh) {  // two halves of k (16 each) to bound registers
+    double av[4][4], bv[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = kh * 16 + 4 * k + s4;
+        av[k][t] = __ldcg(a + (int64_t)kk * lda + t * 8 + q);
+        bv[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * ldb + kk);
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[k][tr], bv[k][tc]);
+  }
+}
+
+// Single-CTA inverse of a factored diagonal tile for the look-ahead stream
+// (where only one SM is free): Linv = L^{-1} by block diagonals.  Diagonal
+// d holds the blocks (j + d, j); each is
+//   Linv[j+d][j] = -Dinv_{j+d} * sum_{m=j}^{j+d-1} L[j+d][m] Linv[m][j]
+// and only needs diagonals < d, so all blocks of a diagonal are independent:
+// one warp per 32x32 block, 4x4 DMMA tiles, 64 fragment loads (L2: the tile
+// was just factored) in flight per 128 DMMAs.
+static __device__ __noinline__ void tri_inv_diag_device(const double* __restrict__ L, const double* __restrict__ dinv, int b,
+                                    double* __restrict__ Linv, double* S, int tid, int bar) {
+  // S: per warp one 32x32 partial sum, [(w*32 + r)*33 + c]
+  const int nbk = b / NB;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int nw = TINV_THREADS / 32;
+  const int q = lane >> 2, s4 = lane & 3;
+  // block diagonal = Dinv, strictly upper blocks = 0 (below is written per diagonal)
+  for (int idx = tid; idx < b * b; idx += TINV_THREADS) {
+    const int c = idx / b, r = idx % b;
+    const int bi = r / NB, bj = c / NB;
+    if (bi < bj) Linv[idx] = 0.0;
+    else if (bi == bj) Linv[idx] = __ldcg(dinv + (int64_t)bj * NB * NB + (c % NB) * NB + (r % NB));
+  }
+  __threadfence_block();
+  named_bar_sync(bar, TINV_THREADS);
+  double* Sw = S + (size_t)warp * NB * 33;
+  for (int d = 1; d < nbk; ++d) {
+    for (int j = warp; j < nbk - d; j += nw) {
+      const int i = j + d;
+      double acc[4][4][2];
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+      // S = sum_m L[i][m] Linv[m][j]
+      for (int m = j; m < i; ++m)
+        block_mma32(acc, L + (int64_t)(m * NB) * b + i * NB, b, Linv + (int64_t)(j * NB) * b + m * NB, b, lane);
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) {
+          Sw[(tr * 8 + q) * 33 + tc * 8 + 2 * s4] = acc[tr][tc][0];
+          Sw[(tr * 8 + q) * 33 + tc * 8 + 2 * s4 + 1] = acc[tr][tc][1];
+          acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+        }
+      __syncwarp();
+      // Linv[i][j] = -Dinv_i S   (Dinv column-major 32x32; S row-major, ld 33)
+      const double* Di = dinv + (int64_t)i * NB * NB;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          av[t] = __ldcg(Di + (4 * k + s4) * NB + t * 8 + q);
+          bv[t] = Sw[(4 * k + s4) * 33 + t * 8 + q];
+        }
+#pragma unroll
+        for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+          for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[tr], bv[tc]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) {
+          const int row = i * NB + tr * 8 + q, col = j * NB + tc * 8 + 2 * s4;
+          Linv[(int64_t)col * b + row] = -acc[tr][tc][0];
+          Linv[(int64_t)(col + 1) * b + row] = -acc[tr][tc][1];
+        }
+    }
+    __threadfence_block();
+    named_bar_sync(bar, TINV_THREADS);  // diagonal d complete before d + 1 reads it
+  }
+}
+
+
+}  // namespace bgp
