@@ -193,6 +193,19 @@ int bgp_sub(bgp_ctx_t ctx, const double* a, const double* b, double* out,
  * bgp_tile_update: C -= A B^T over a list of `count` (C, A, B) tile index
  *   triples into three packed-tile bases (kernels.py:188-192); a triple with
  *   lower != 0 updates only the lower triangle (diagonal SYRK). */
+/* Stream-ordered forms for the multi-GPU schedule (no host synchronization
+ * per step): bgp_tile_potrf_async factors a diagonal tile and, when linv is
+ * not null, writes its inverse (b x b column-major); a failing pivot is
+ * recorded in the context's device status, which bgp_info_reset clears and
+ * bgp_info_read returns (synchronizing).  bgp_panel_trsm_inv solves `count`
+ * consecutive tiles in place, A <- A Linv^T, on the DMMA GEMM; it is skipped
+ * once the status records a failure. */
+int bgp_info_reset(bgp_ctx_t ctx, void* stream);
+int bgp_info_read(bgp_ctx_t ctx, int64_t* info, void* stream);
+int bgp_tile_potrf_async(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0,
+                         double* linv, void* stream);
+int bgp_panel_trsm_inv(bgp_ctx_t ctx, const double* linv, double* A, int64_t count,
+                       int tile, void* stream);
 /* bgp_tile_potrf_inv: bgp_tile_potrf (row0 = 0) followed by the one-CTA
  * inverse the look-ahead uses: linv (b x b column-major) = L^{-1}. */
 int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv,

@@ -67,6 +67,10 @@ SIGNATURES = {
     "bgp_sub": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _i64, _c_dp]),
     "bgp_tile_potrf": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, ctypes.POINTER(_i64), _c_dp]),
     "bgp_tile_potrf_inv": (_int, [ctypes.c_void_p, _c_dp, _int, _c_dp, ctypes.POINTER(_i64), _c_dp]),
+    "bgp_info_reset": (_int, [ctypes.c_void_p, _c_dp]),
+    "bgp_info_read": (_int, [ctypes.c_void_p, ctypes.POINTER(_i64), _c_dp]),
+    "bgp_tile_potrf_async": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, _c_dp, _c_dp]),
+    "bgp_panel_trsm_inv": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_construct_tiles": (_int, [ctypes.c_void_p, ctypes.POINTER(Generator), _c_dp, _i64, _int, _int,

@@ -614,6 +614,35 @@ int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv, 
   return read_info(ctx, s, info);
 }
 
+int bgp_info_reset(bgp_ctx_t ctx, void* stream) { return reset_info(ctx, (cudaStream_t)stream); }
+
+int bgp_info_read(bgp_ctx_t ctx, int64_t* info, void* stream) { return read_info(ctx, (cudaStream_t)stream, info); }
+
+int bgp_tile_potrf_async(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0, double* linv, void* stream) {
+  if (!valid_tile(tile)) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
+  int rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
+  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s))) return rc;
+  if (linv) return launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s, nullptr, true);
+  return BGP_OK;
+}
+
+int bgp_panel_trsm_inv(bgp_ctx_t ctx, const double* linv, double* A, int64_t count, int tile, void* stream) {
+  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
+  if (count == 0) return BGP_OK;
+  GemmProblem p{};
+  p.mode = GEMM_TRSM_PANEL;
+  p.b = tile;
+  p.count = count;
+  p.panel0 = 0;
+  p.alpha = 1.0;
+  p.beta = 0.0;
+  p.check_info = true;
+  return launch_gemm(ctx, p, A, A, count, A, count, count, (cudaStream_t)stream, linv);
+}
+
 int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, int tile, void* stream) {
   if (!valid_tile(tile)) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

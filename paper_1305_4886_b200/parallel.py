@@ -127,25 +127,31 @@ def dist_cholesky(dist, local, ops, comm):
 
     `local` is this rank's (count, b, b) tile stack.  Returns the first
     failing pivot row (1-based, LAPACK info) agreed by all ranks, or 0.
+
+    Per step J the owner of (J, J) factors it and inverts it; the inverse is
+    broadcast and the ranks of process column J mod Pc solve their panel tiles
+    as A <- A Linv^T (the DMMA GEMM on the GPU).  The update items of every
+    step are built and uploaded once, and pivot failures stay in the device
+    status until the end, so the host never waits on the GPU inside the loop.
     """
     b, T, me = dist.b, dist.T, dist.rank
-    diag_buf = ops.empty((b, b))
+    inv_buf = ops.empty((b, b))
+    ops.begin()
     info = 0
     panel = None
+    layouts = [dist.panel_layout(J) for J in range(T - 1)]
+    items = ops.prepare_items([dist.update_items(J, layouts[J][1]) for J in range(T - 1)])
     for J in range(T):
         d = dist.owner(J, J)
         if me == d:
-            k = dist.local[(J, J)]
-            if info == 0:
-                info = ops.potrf(local, k, J * b)
-            ops.copy_tile(diag_buf, local, k)
-        comm.broadcast(diag_buf, d)
+            info = info or ops.potrf_factor(local, dist.local[(J, J)], J * b, inv_buf if J + 1 < T else None)
         if J + 1 >= T:
             break
+        comm.broadcast(inv_buf, d)
         s, c = dist.my_panel(J)
         if c:
-            ops.trsm(diag_buf, local, s, c)
-        chunks, slot, ntot = dist.panel_layout(J)
+            ops.trsm_inv(inv_buf, local, s, c)
+        chunks, slot, ntot = layouts[J]
         if panel is None or panel.shape[0] < ntot:
             panel = ops.empty((max(ntot, 1), b, b))
         for root, off, cnt in chunks:
@@ -157,9 +163,8 @@ def dist_cholesky(dist, local, ops, comm):
                 assert pcount == cnt
                 ops.copy_tiles(view, local, ps, cnt)
             comm.broadcast(view, root)
-        items = dist.update_items(J, slot)
-        if len(items):
-            ops.update(local, panel, items)
+        ops.update(local, panel, items[J])
+    info = ops.end(info)
     return comm.min_nonzero(info)
 
 
@@ -261,6 +266,22 @@ class LibTileOps:
         return ctypes.c_void_p(t.data_ptr())
 
     # tile kernels ------------------------------------------------------------
+    def begin(self):
+        self.cl.call("bgp_info_reset", self.cl.stream)
+
+    def end(self, info):
+        import ctypes
+        dev = ctypes.c_int64(0)
+        self.cl.call("bgp_info_read", ctypes.byref(dev), self.cl.stream)
+        return int(info or dev.value)
+
+    def potrf_factor(self, local, k, row0, inv):
+        """Factor tile k in place and (inv not None) write its inverse; the
+        status stays on the device until end()."""
+        self.cl.call("bgp_tile_potrf_async", self._p(local[k]), self.b, row0,
+                     self._p(inv) if inv is not None else None, self.cl.stream)
+        return 0
+
     def potrf(self, local, k, row0):
         import ctypes
         info = ctypes.c_int64(0)
@@ -274,14 +295,35 @@ class LibTileOps:
     def copy_tiles(self, dst, local, start, count):
         dst.copy_(local[start:start + count])
 
+    def trsm_inv(self, inv, local, start, count):
+        self.cl.call("bgp_panel_trsm_inv", self._p(inv), self._p(local[start]), count, self.b,
+                     self.cl.stream)
+
     def trsm(self, diag, local, start, count):
         self.cl.call("bgp_panel_trsm", self._p(diag), self._p(local[start]), count, self.b,
                      self.cl.stream)
 
+    def prepare_items(self, per_step):
+        """Upload the update items of every step at once; returns per-step
+        (device view, count)."""
+        flat = [np.asarray(a, dtype=np.int32).reshape(-1, 4) for a in per_step]
+        total = np.concatenate(flat) if flat and sum(len(a) for a in flat) else np.zeros((1, 4), np.int32)
+        dev = self._items(total)
+        out, off = [], 0
+        for a in flat:
+            out.append((dev[4 * off:4 * (off + len(a))], len(a)))
+            off += len(a)
+        return out
+
     def update(self, local, panel, items):
-        dev = self._items(items)
+        if isinstance(items, tuple):
+            dev, count = items
+        else:
+            dev, count = self._items(items), len(items)
+        if count == 0:
+            return
         self.cl.call("bgp_tile_update", self._p(local), self._p(panel), self._p(panel),
-                     self._p(dev), len(items), self.b, self.cl.stream)
+                     self._p(dev), count, self.b, self.cl.stream)
 
     def sub_into(self, out, a, b):
         self.cl.call("bgp_sub", self._p(a), self._p(b), self._p(out), out.numel(), self.cl.stream)

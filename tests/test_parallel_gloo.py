@@ -43,6 +43,27 @@ class NumpyTileOps:
         M[:] = L
         return 0
 
+    def begin(self):
+        pass
+
+    def end(self, info):
+        return info
+
+    def potrf_factor(self, local, k, row0, inv):
+        info = self.potrf(local, k, row0)
+        if info == 0 and inv is not None:
+            self._m(inv)[:] = np.linalg.inv(np.tril(self._m(local[k])))
+        return info
+
+    def trsm_inv(self, inv, local, start, count):
+        Li = self._m(inv)
+        for t in range(start, start + count):
+            M = self._m(local[t])
+            M[:] = M @ Li.T
+
+    def prepare_items(self, per_step):
+        return [np.asarray(a).reshape(-1, 4) for a in per_step]
+
     def copy_tile(self, dst, local, k):
         dst.copy_(local[k])
 
