@@ -220,6 +220,8 @@ int bgp_construct_tiles(bgp_ctx_t ctx, const bgp_generator* gen, const double* X
                         int64_t count, double* out, void* stream);
 /* Diagonal-tile solve of a distributed TRSV step: x (b doubles) <- L_jj^{-1} x
  * or L_jj^{-T} x; row0 = global row of the tile (kernels.py:244-249). */
+/* bgp_tile_trsv with info == NULL: stream-ordered, the status stays in the
+ * device (bgp_info_read). */
 int bgp_tile_trsv(bgp_ctx_t ctx, const double* Ljj, int tile, int64_t row0,
                   int64_t n, double* x, int trans, int64_t* info, void* stream);
 /* acc[target*b ...] += L_tile x_J (trans 0) or L_tile^T x_J (trans 1) for

@@ -563,8 +563,9 @@ int bgp_tile_trsv(bgp_ctx_t ctx, const double* Ljj, int tile, int64_t row0, int6
                   int64_t* info, void* stream) {
   if (!valid_tile(tile)) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = reset_info(ctx, s);
-  if (rc) return rc;
+  int rc;
+  if (!info) return launch_tile_trsv(ctx, Ljj, tile, row0, n, x, trans, s);  // stream-ordered form
+  if ((rc = reset_info(ctx, s))) return rc;
   if ((rc = launch_tile_trsv(ctx, Ljj, tile, row0, n, x, trans, s))) return rc;
   return read_info(ctx, s, info);
 }

@@ -175,21 +175,22 @@ def dist_trsv(dist, local, y, ops, comm, forward=True):
     b, T, me = dist.b, dist.T, dist.rank
     acc = ops.zeros((T * b,))
     x = ops.zeros((T * b,))
+    ops.begin()
     info = 0
-    order = range(T) if forward else range(T - 1, -1, -1)
-    for J in order:
+    order = list(range(T)) if forward else list(range(T - 1, -1, -1))
+    per_step = [dist.column_items(J) if forward else dist.row_items(J) for J in order]
+    dev_items = ops.prepare_gemv_items(per_step)
+    for J, items in zip(order, dev_items):
         d = dist.owner(J, J)
         blk = acc[J * b:(J + 1) * b]
         comm.reduce_sum(blk, d)
         xJ = x[J * b:(J + 1) * b]
         if me == d:
             ops.sub_into(xJ, y[J * b:(J + 1) * b], blk)
-            if info == 0:
-                info = ops.tile_trsv(local, dist.local[(J, J)], J * b, xJ, 0 if forward else 1)
+            info = info or ops.tile_trsv(local, dist.local[(J, J)], J * b, xJ, 0 if forward else 1)
         comm.broadcast(xJ, d)
-        items = dist.column_items(J) if forward else dist.row_items(J)
-        if len(items):
-            ops.gemv(local, items, xJ, acc, 0 if forward else 1)
+        ops.gemv(local, items, xJ, acc, 0 if forward else 1)
+    info = ops.end(info)
     return x, comm.min_nonzero(info)
 
 
@@ -329,15 +330,29 @@ class LibTileOps:
         self.cl.call("bgp_sub", self._p(a), self._p(b), self._p(out), out.numel(), self.cl.stream)
 
     def tile_trsv(self, local, k, row0, x, trans):
-        import ctypes
-        info = ctypes.c_int64(0)
-        self.cl.call("bgp_tile_trsv", self._p(local[k]), self.b, row0, self.n, self._p(x), trans,
-                     ctypes.byref(info), self.cl.stream)
-        return int(info.value)
+        """Stream-ordered: a zero pivot stays in the device status (end())."""
+        self.cl.call("bgp_tile_trsv", self._p(local[k]), self.b, row0, self.n, self._p(x), trans, None,
+                     self.cl.stream)
+        return 0
+
+    def prepare_gemv_items(self, per_step):
+        flat = [np.asarray(a, dtype=np.int32).reshape(-1, 2) for a in per_step]
+        total = np.concatenate(flat) if flat and sum(len(a) for a in flat) else np.zeros((1, 2), np.int32)
+        dev = self._items(total)
+        out, off = [], 0
+        for a in flat:
+            out.append((dev[2 * off:2 * (off + len(a))], len(a)))
+            off += len(a)
+        return out
 
     def gemv(self, local, items, xJ, acc, trans):
-        dev = self._items(items)
-        self.cl.call("bgp_tile_gemv", self._p(local), self._p(dev), len(items), self.b,
+        if isinstance(items, tuple):
+            dev, count = items
+        else:
+            dev, count = self._items(items), len(items)
+        if count == 0:
+            return
+        self.cl.call("bgp_tile_gemv", self._p(local), self._p(dev), count, self.b,
                      self._p(xJ), self._p(acc), trans, self.cl.stream)
 
     def logdet_partial(self, local, diag):

@@ -64,6 +64,9 @@ class NumpyTileOps:
     def prepare_items(self, per_step):
         return [np.asarray(a).reshape(-1, 4) for a in per_step]
 
+    def prepare_gemv_items(self, per_step):
+        return [np.asarray(a).reshape(-1, 2) for a in per_step]
+
     def copy_tile(self, dst, local, k):
         dst.copy_(local[k])
 
