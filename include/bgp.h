@@ -116,6 +116,12 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
  * Compute) runs the same kernels one after another on `stream`. */
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile,
               int64_t* info, void* stream);
+/* With 512 tiles and more than 2*tiles tile rows, bgp_potrf finishes the last
+ * `tiles` tile rows on 256 tiles (the serial panel chain is ~4x shorter
+ * there), and with 256 tiles the last tiles/2 rows on 128: the trailing
+ * triangle is re-tiled into context scratch, factored, and copied back.
+ * Default 32 (or BGP_TAIL in the environment); 0 disables. */
+int bgp_set_tail(bgp_ctx_t ctx, int tiles);
 
 /* ---- K3 solves -------------------------------------------------------------
  * bgp_trsv replaces distla.solve_vector (bg/distla/kernels.py:200-250):

@@ -43,6 +43,9 @@ struct Ctx {
   size_t linv_cap = 0;
   int* d_queue = nullptr;  // task counter of standalone GEMM launches
   size_t queue_cap = 0;
+  double* d_tail[2] = {nullptr, nullptr};  // re-tiled trailing triangles of the Cholesky tail
+  size_t tail_cap[2] = {0, 0};
+  int tail_tiles = 32;  // 512-tile rows finished on 256 tiles (half as many 256 rows on 128; bgp_set_tail)
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)
   bool profile = false;

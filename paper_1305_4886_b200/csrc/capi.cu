@@ -130,6 +130,7 @@ const char* bgp_version(void) { return "libbgp 0.1 sm_100a (FP64 DMMA + TMA)"; }
 int bgp_init(int device, bgp_ctx_t* out) {
   bgp_ctx* ctx = new bgp_ctx();
   ctx->device = device;
+  if (const char* e = getenv("BGP_TAIL")) ctx->tail_tiles = atoi(e);
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_info, 64);
@@ -169,6 +170,8 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_sync) cudaFree(ctx->d_sync);
   if (ctx->d_gate) cudaFree(ctx->d_gate);
   if (ctx->d_linv) cudaFree(ctx->d_linv);
+  for (int l = 0; l < 2; ++l)
+    if (ctx->d_tail[l]) cudaFree(ctx->d_tail[l]);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
   delete[] ctx->events;
   delete ctx;
@@ -209,14 +212,35 @@ static int diag_tile_blocks(int b) {
 // the trailing update.  Waits are one-way (update blocks -> POTRF -> TRSM
 // tasks, never back), bounded, and reported as errors if they time out.  The
 // only host synchronization is the final status read.
-int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
-  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int b = tile;
+// Event marks of one bgp_potrf call (profiling only).
+struct Marks {
+  Ctx* ctx;
+  int ev = 0;
+  int mark(cudaStream_t st) {
+    if (!ctx->profile || ev >= ctx->events_cap) return -1;
+    cudaEventRecord(ctx->events[ev], st);
+    return ev++;
+  }
+  double el(int a, int c) const {
+    float ms = 0.f;
+    if (a >= 0 && c >= 0) cudaEventElapsedTime(&ms, ctx->events[a], ctx->events[c]);
+    return (double)ms;
+  }
+};
+
+struct StepMarks {
+  int gemm_end, p0, p1, t_end;
+};
+
+// Panels 0 .. J_stop-1 of the packed triangle `tiles` (T tile rows of b):
+// factor them and apply their updates to the trailing matrix (tiles R, C >=
+// J_stop).  J_stop = T is the whole factorization.  Pivot rows are reported
+// as row_base + row.  Steps are recorded in sm_out for profiling.
+static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, int J_stop, int64_t row_base,
+                     Marks& mk, StepMarks* sm_out, int* m_first, int* m_p0_out, int* m_t0_out) {
   const int T = (int)((n + b - 1) / b);
   const int nbk = b / 32;
-  int rc = reset_info(ctx, s);
-  if (rc) return rc;
+  int rc;
   const size_t dinv_bytes = (size_t)nbk * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
@@ -228,12 +252,10 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
     if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
   }
-  gemm_prepare();
-  potrf_prepare();
   const int64_t ntiles = tri_count(T);
   const int64_t tsz = (int64_t)b * b;
-  const int nblk = (b / 128) * (b / 64);                 // 128x64 blocks per tile (gemm.cu)
-  const int diag_need = diag_tile_blocks(b) * 4;         // 4 warps per block (gemm.cu GROUP_WARPS)
+  const int nblk = (b / 128) * (b / 64);          // 128x64 blocks per tile (gemm.cu)
+  const int diag_need = diag_tile_blocks(b) * 4;  // 4 warps per block (gemm.cu GROUP_WARPS)
   const int tile_need = nblk * 4;
   // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead inside the update
   // launch; 0 sequential launches on all SMs; 2 sequential with the update on
@@ -243,30 +265,10 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     if (const char* e = getenv("BGP_LOOKAHEAD")) return atoi(e);
     return 1;
   }();
-  // profiling: marks on the caller's stream around every launch
-  const int nev = 3 * T + 8;
-  if (ctx->profile && ctx->events_cap < nev) {
-    for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
-    delete[] ctx->events;
-    ctx->events = new cudaEvent_t[nev];
-    for (int i = 0; i < nev; ++i) cudaEventCreate(&ctx->events[i]);
-    ctx->events_cap = nev;
-  }
-  int ev = 0;
-  auto mark = [&](cudaStream_t st) -> int {
-    if (!ctx->profile || ev >= ctx->events_cap) return -1;
-    cudaEventRecord(ctx->events[ev], st);
-    return ev++;
-  };
-  auto el = [&](int a, int c) -> double {
-    float ms = 0.f;
-    if (a >= 0 && c >= 0) cudaEventElapsedTime(&ms, ctx->events[a], ctx->events[c]);
-    return (double)ms;
-  };
   // tri_inv of K (needed when panel K has tiles below the diagonal)
-  auto inverse = [&](int K, cudaStream_t st, int* done) -> int {
+  auto inverse = [&](int K) -> int {
     if (K + 1 >= T) return BGP_OK;
-    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, st, done, true);
+    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, s, nullptr, true);
   };
   // standalone panel solve of K on the caller's stream
   auto panel_solve = [&](int K) -> int {
@@ -283,19 +285,15 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     p.check_info = true;
     return launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv);
   };
-  struct StepMarks {
-    int gemm_end, p0, p1, t_end;
-  };
-  static thread_local StepMarks sm_[4096];
 
-  const int m_start = mark(s);
-  if ((rc = launch_tile_potrf(ctx, tiles, b, 0, ctx->d_dinv, s))) return rc;
-  if ((rc = inverse(0, s, nullptr))) return rc;
-  const int m_p0 = mark(s);
+  *m_first = mk.mark(s);
+  if ((rc = launch_tile_potrf(ctx, tiles, b, row_base, ctx->d_dinv, s))) return rc;
+  if ((rc = inverse(0))) return rc;
+  *m_p0_out = mk.mark(s);
   if ((rc = panel_solve(0))) return rc;
-  const int m_t0 = mark(s);
-  int m_last = m_t0;
-  for (int J = 0; J + 1 < T; ++J) {
+  *m_t0_out = mk.mark(s);
+  const int J_last = J_stop < T ? J_stop : T - 1;  // updates with panels 0 .. J_last-1
+  for (int J = 0; J < J_last; ++J) {
     const int K = J + 1;  // next panel
     double* dkk = tiles + tri_index(K, K, T) * tsz;
     int* gate = ctx->d_gate + (int64_t)J * stride;
@@ -309,78 +307,167 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     p.beta = 1.0;
     p.check_info = true;
     p.queue = gate + stride - 2;
+    const bool next = K < J_stop;  // panel K is factored here
     if (la_mode == 1) {
-      // POTRF(K) (+ inverse) by the launch's last CTA, the TRSM of panel K as
-      // gated tasks of the same launch
-      p.col_gate = gate;
-      p.trsm_next = (K + 1 < T);
-      p.tile_need = tile_need;
-      p.linv_flag = gate + T;
-      p.linv_need = nbk;
-      p.trsm_tail = 12 * ctx->num_sms;  // ~6 update blocks per consumer group
-      p.potrf_tile = dkk;
-      p.potrf_row0 = (int64_t)K * b;
-      p.dinv = ctx->d_dinv;
-      p.linv = ctx->d_linv;
-      p.diag_need = diag_need;
+      if (next) {
+        // POTRF(K) (+ inverse) by the launch's last CTA, the TRSM of panel K
+        // as gated tasks of the same launch
+        p.col_gate = gate;
+        p.trsm_next = (K + 1 < T);
+        p.tile_need = tile_need;
+        p.linv_flag = gate + T;
+        p.linv_need = nbk;
+        p.trsm_tail = 12 * ctx->num_sms;  // ~6 update blocks per consumer group
+        p.potrf_tile = dkk;
+        p.potrf_row0 = row_base + (int64_t)K * b;
+        p.dinv = ctx->d_dinv;
+        p.linv = ctx->d_linv;
+        p.diag_need = diag_need;
+      }
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
-      sm.gemm_end = mark(s);
+      sm.gemm_end = sm.t_end = mk.mark(s);
     } else {
       p.grid_limit = la_mode == 2 ? ctx->num_sms - 1 : 0;
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s))) return rc;
-      sm.gemm_end = mark(s);
-      sm.p0 = sm.gemm_end;
-      if ((rc = launch_tile_potrf(ctx, dkk, b, (int64_t)K * b, ctx->d_dinv, s))) return rc;
-      if ((rc = inverse(K, s, nullptr))) return rc;
-      sm.p1 = mark(s);
-      if ((rc = panel_solve(K))) return rc;
-      sm.t_end = mark(s);
-      if (J < 4096) sm_[J] = sm;
-      m_last = sm.t_end;
-      continue;
+      sm.gemm_end = sm.p0 = mk.mark(s);
+      if (next) {
+        if ((rc = launch_tile_potrf(ctx, dkk, b, row_base + (int64_t)K * b, ctx->d_dinv, s))) return rc;
+        if ((rc = inverse(K))) return rc;
+      }
+      sm.p1 = mk.mark(s);
+      if (next && (rc = panel_solve(K))) return rc;
+      sm.t_end = mk.mark(s);
     }
-    if (J < 4096) sm_[J] = sm;
-    m_last = sm.gemm_end;
+    if (sm_out && J < 4096) sm_out[J] = sm;
   }
-  const int m_wait = -1;
+  return BGP_OK;
+}
+
+// Copy the trailing triangle of tile rows J0.. of a packed b-tile triangle
+// (T tile rows) to / from a packed (b/2)-tile triangle of T2 tile rows.
+__global__ void retile_kernel(double* __restrict__ big, int T, int b, int J0, double* __restrict__ half, int T2,
+                              int to_half) {
+  int r2, c2;
+  tri_decode(blockIdx.x, T2, r2, c2);
+  const int h = b / 2;
+  const int64_t bt = tri_index(J0 + r2 / 2, J0 + c2 / 2, T);
+  double* src = big + bt * (int64_t)b * b + (int64_t)((c2 & 1) * h) * b + (r2 & 1) * h;
+  double* dst = half + (int64_t)blockIdx.x * h * h;
+  for (int idx = threadIdx.x; idx < h * h; idx += blockDim.x) {
+    const int c = idx / h, r = idx % h;
+    if (to_half) dst[idx] = src[(int64_t)c * b + r];
+    else src[(int64_t)c * b + r] = dst[idx];
+  }
+}
+
+// Factor a packed triangle of b tiles: panels on b tiles while the trailing
+// matrix is large, then the last tile rows re-tiled to b/2 and finished
+// there (recursively, down to 128): the tail is bound by the serial POTRF +
+// inverse chain, which is ~4x shorter per halving of the tile.
+static int potrf_level(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, int64_t row_base, int level,
+                       Marks& mk, StepMarks* sm_out, int* m_first, int* m_p0, int* m_t0, int* J0_out,
+                       int* m_tail_end) {
+  const int T = (int)((n + b - 1) / b);
+  const int tail = b == 512 ? ctx->tail_tiles : (b == 256 ? ctx->tail_tiles / 2 : 0);
+  const int J0 = (b >= 256 && tail > 0 && T > 2 * tail && level < 2) ? T - tail : T;
+  *J0_out = J0;
+  int rc = potrf_run(ctx, tiles, n, b, s, J0, row_base, mk, sm_out, m_first, m_p0, m_t0);
+  if (rc || J0 == T) return rc;
+  const int64_t n2 = n - (int64_t)J0 * b;
+  const int b2 = b / 2, T2 = (int)((n2 + b2 - 1) / b2);
+  if ((rc = ensure(ctx, (void**)&ctx->d_tail[level], &ctx->tail_cap[level],
+                   (size_t)tri_count(T2) * b2 * b2 * sizeof(double))))
+    return rc;
+  double* sub = ctx->d_tail[level];
+  retile_kernel<<<(unsigned)tri_count(T2), 256, 0, s>>>(tiles, T, b, J0, sub, T2, 1);
+  ctx->launches++;
+  if ((rc = check_launch(ctx, "retile"))) return rc;
+  int a0, a1, a2, j0, te;
+  if ((rc = potrf_level(ctx, sub, n2, b2, s, row_base + (int64_t)J0 * b, level + 1, mk, nullptr, &a0, &a1, &a2,
+                        &j0, &te)))
+    return rc;
+  retile_kernel<<<(unsigned)tri_count(T2), 256, 0, s>>>(tiles, T, b, J0, sub, T2, 0);
+  ctx->launches++;
+  if ((rc = check_launch(ctx, "retile"))) return rc;
+  *m_tail_end = mk.mark(s);
+  return BGP_OK;
+}
+
+int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int b = tile;
+  const int T = (int)((n + b - 1) / b);
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  gemm_prepare();
+  potrf_prepare();
+  // profiling events (all levels)
+  const int nev = 6 * T + 64;
+  if (ctx->profile && ctx->events_cap < nev) {
+    for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
+    delete[] ctx->events;
+    ctx->events = new cudaEvent_t[nev];
+    for (int i = 0; i < nev; ++i) cudaEventCreate(&ctx->events[i]);
+    ctx->events_cap = nev;
+  }
+  Marks mk{ctx};
+  static thread_local StepMarks sm_[4096];
+  int m_start, m_p0, m_t0, J0, m_tail_end = -1;
+  if ((rc = potrf_level(ctx, tiles, n, b, s, 0, 0, mk, sm_, &m_start, &m_p0, &m_t0, &J0, &m_tail_end))) return rc;
+  const int64_t n2 = n - (int64_t)J0 * b;
   rc = read_info(ctx, s, info);
   if (rc == BGP_OK && info && (unsigned long long)*info >= BGP_INFO_DATAFLOW_TIMEOUT) {
     ctx->err = "look-ahead wait timed out (internal dependency error)";
     return BGP_E_CUDA;
   }
   if (rc == BGP_OK && ctx->profile) {
-    ctx->prof[0] += el(m_start, m_p0);  // potrf(0) + inverse: on the critical path
-    ctx->prof[9] += el(m_start, m_p0);
+    static const int la1 = [] {
+      const char* e = getenv("BGP_LOOKAHEAD");
+      return e ? atoi(e) : 1;
+    }();
+    ctx->prof[0] += mk.el(m_start, m_p0);  // potrf(0) + inverse: on the critical path
+    ctx->prof[9] += mk.el(m_start, m_p0);
     ctx->prof[5] += 1;
-    ctx->prof[1] += el(m_p0, m_t0);  // trsm(0)
+    ctx->prof[1] += mk.el(m_p0, m_t0);  // trsm(0)
     ctx->prof[6] += 1;
     int prev = m_t0;
-    for (int J = 0; J + 1 < T && J < 4096; ++J) {
+    const int nsteps = (J0 < T ? J0 : T - 1);
+    for (int J = 0; J < nsteps && J < 4096; ++J) {
       const StepMarks& m = sm_[J];
       const double kk = (double)(T - J - 1);
-      if (J < 4096) ctx->step_ms[J] = el(prev, m.gemm_end);
-      if (la_mode == 1) {
-        ctx->prof[2] += el(prev, m.gemm_end);  // update + POTRF / inverse / TRSM of the next panel
-        ctx->prof[4] += (double)b * b * b * (kk * kk + (kk - 1.0));
-        prev = m.gemm_end;
+      ctx->step_ms[J] = mk.el(prev, m.t_end);
+      ctx->prof[2] += mk.el(prev, m.gemm_end);
+      if (la1 == 1) {
+        ctx->prof[4] += (double)b * b * b * (kk * kk + (J + 1 < J0 ? kk - 1.0 : 0.0));
       } else {
-        ctx->prof[2] += el(prev, m.gemm_end);
-        ctx->prof[0] += el(m.p0, m.p1);
-        ctx->prof[9] += el(m.p0, m.p1);
-        ctx->prof[1] += el(m.p1, m.t_end);
+        ctx->prof[0] += mk.el(m.p0, m.p1);
+        ctx->prof[9] += mk.el(m.p0, m.p1);
+        ctx->prof[1] += mk.el(m.p1, m.t_end);
         ctx->prof[6] += 1;
         ctx->prof[4] += (double)b * b * b * kk * kk;
-        prev = m.t_end;
       }
+      prev = m.t_end;
       ctx->prof[3] += 1;
       ctx->prof[5] += 1;
     }
-    if (m_wait >= 0) ctx->prof[9] += el(m_last, m_wait);
-    ctx->prof[8] += el(m_start, m_wait >= 0 ? m_wait : m_last);
+    if (m_tail_end >= 0) {  // the re-tiled tail: its flops, n2^3/3, counted with the update
+      ctx->step_ms[nsteps < 4096 ? nsteps : 4095] = mk.el(prev, m_tail_end);
+      ctx->prof[2] += mk.el(prev, m_tail_end);
+      ctx->prof[4] += (double)n2 * n2 * n2 / 3.0;
+      prev = m_tail_end;
+    }
+    ctx->prof[8] += mk.el(m_start, prev);
     ctx->prof[7] += 1;
-    ctx->nsteps = T - 1 < 4096 ? T - 1 : 4096;
+    ctx->nsteps = nsteps < 4096 ? nsteps : 4096;
   }
   return rc;
+}
+
+int bgp_set_tail(bgp_ctx_t ctx, int tiles) {
+  if (tiles < 0) return BGP_E_ARG;
+  ctx->tail_tiles = tiles;
+  return BGP_OK;
 }
 
 int bgp_set_profiling(bgp_ctx_t ctx, int on) {

@@ -84,3 +84,35 @@ def test_tile_inverse(cluster_factory, tile):
     got = linv.cpu().numpy().T  # column-major -> row-major
     assert relerr(got, np.linalg.inv(L)) <= 1e-12
     assert np.all(np.triu(got, 1) == 0.0)
+
+
+@pytest.mark.parametrize("tail,n", [(2, 512 * 7 - 100), (3, 512 * 9 - 7), (4, 512 * 9)])
+def test_tail_retiling_matches_lapack(cluster_factory, tail, n):
+    """512-tile factorization whose last `tail` tile rows are re-tiled to 256."""
+    from paper_1305_4886_b200 import distla
+    cl = cluster_factory(tile=512)
+    assert cl.lib.bgp_set_tail(cl._ctx, tail) == 0
+    for A in (spd_matrix(n, seed=n), _cov(n, seed=n)):
+        C = distla.distribute(cl, "C", A, "triangular", distla.make_layout(n, cl.grid, h=2))
+        L, _ = distla.distributed_cholesky(cl, C, "L")
+        got = distla.collect(cl, L)
+        assert relerr(got, np.linalg.cholesky(A)) <= 1e-12
+        assert abs(distla.log_det_from_chol(cl, L) - np.linalg.slogdet(A)[1]) <= 1e-10 * abs(np.linalg.slogdet(A)[1])
+        cl.remote_rm("L")
+
+
+def test_tail_failure_row(cluster_factory):
+    """A non-positive pivot inside the re-tiled tail reports its global row."""
+    from paper_1305_4886_b200 import distla
+    from paper_1305_4886_b200.errors import NotPositiveDefinite
+    n = 512 * 7
+    A = spd_matrix(n, seed=9)
+    bad = 512 * 6 + 300  # inside the last two tile rows (tail = 2)
+    A[bad, bad] = -1.0
+    cl = cluster_factory(tile=512)
+    cl.lib.bgp_set_tail(cl._ctx, 2)
+    lay = distla.make_layout(n, cl.grid, h=7)
+    C = distla.distribute(cl, "C", A, "triangular", lay)
+    with pytest.raises(NotPositiveDefinite) as info:
+        distla.distributed_cholesky(cl, C, "L")
+    assert info.value.block_index == bad // lay.block_size + 1
