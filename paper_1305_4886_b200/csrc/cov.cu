@@ -77,9 +77,35 @@ __device__ __forceinline__ double gen_eval(const GenDev& g, const double* xi, co
 
 constexpr int kCovThreads = 256;
 
+// Specialised correlation for the common generators in 2-D (KIND 1..3:
+// Matern nu = 1/2, 3/2, 5/2; KIND 4: squared exponential), same operation
+// order as gen_eval (numpy's), without the per-entry family / dimension
+// dispatch; KIND 0 is the generic path.
+// x / rho through the reciprocal with one residual correction: the correctly
+// rounded quotient for all but rare ties (vs __ddiv_rn's special-case path)
+__device__ __forceinline__ double div_rho(double x, double rho, double rinv) {
+  const double q = __dmul_rn(x, rinv);
+  return fma(fma(-q, rho, x), rinv, q);
+}
+
+template <int KIND>
+__device__ __forceinline__ double corr2d(double dx, double dy, const GenDev& g, double rinv) {
+  const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+  if (KIND == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 * (d/rho)**2)
+    const double t = div_rho(dist, g.p[1], rinv);
+    return exp(__dmul_rn(-0.5, __dmul_rn(t, t)));
+  }
+  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) * d / rho
+  const double sv = div_rho(__dmul_rn(g.sqrt2nu, dist), g.p[1], rinv);
+  const double e = exp(-sv);
+  if (KIND == 1) return e;
+  if (KIND == 2) return __dmul_rn(__dadd_rn(1.0, sv), e);
+  return __dmul_rn(__dadd_rn(__dadd_rn(1.0, sv), __ddiv_rn(__dmul_rn(sv, sv), 3.0)), e);
+}
+
 // triangular: one CTA per lower tile (flat packed index, or an explicit
 // (I, J) list for a rank's share of a 2-D block-cyclic distribution)
-template <bool kPts>
+template <bool kPts, int KIND>
 __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const double* __restrict__ X,
                                                               int64_t n, int T, int b,
                                                               double* __restrict__ out,
@@ -100,11 +126,22 @@ __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const do
   }
   __syncthreads();
   double* tile = out + (int64_t)blockIdx.x * b * b;
+  // interior tiles (no padding, off the diagonal): no per-entry checks
+  const bool interior = KIND != 0 && I != J && i0 + b <= n && j0 + b <= n;
   for (int r = threadIdx.x; r < b; r += blockDim.x) {
     const int64_t i = i0 + r;
     double xi[kMaxDim];
 #pragma unroll
     for (int d = 0; d < kMaxDim; ++d) xi[d] = (kPts && d < dim && i < n) ? X[i * dim + d] : 0.0;
+    if (interior) {
+      const double p0 = g.p[0], rinv = 1.0 / g.p[1];
+#pragma unroll 4
+      for (int c = 0; c < b; ++c) {
+        const double dx = xi[0] - colpts[2 * c], dy = xi[1] - colpts[2 * c + 1];
+        tile[(int64_t)c * b + r] = __dmul_rn(p0, corr2d<KIND>(dx, dy, g, rinv));
+      }
+      continue;
+    }
     const int cmax = (I == J) ? r : b - 1;
     for (int c = 0; c < b; ++c) {
       const int64_t j = j0 + c;
@@ -165,15 +202,35 @@ __global__ void cov_vec_kernel(GenDev g, int64_t n, int64_t padded, double* __re
   }
 }
 
+// specialised kernel variant for a generator (see corr2d)
+static int cov_kind(const GenDev& g) {
+  if (g.dim != 2 || (g.part != BGP_PART_COV && g.part != BGP_PART_CROSS && g.part != BGP_PART_PRED)) return 0;
+  if (g.family == BGP_GEN_MATERN && g.nucode >= 0 && g.nucode <= 2) return 1 + g.nucode;
+  if (g.family == BGP_GEN_SQEXP) return 4;
+  return 0;
+}
+
+template <bool kPts>
+static void launch_cov_tri(const GenDev& g, unsigned grid, size_t smem, cudaStream_t s, const double* X, int64_t n,
+                           int T, int b, double* out, const int32_t* tile_ij) {
+  switch (kPts ? cov_kind(g) : 0) {
+    case 1: cov_tri_kernel<kPts, 1><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+    case 2: cov_tri_kernel<kPts, 2><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+    case 3: cov_tri_kernel<kPts, 3><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+    case 4: cov_tri_kernel<kPts, 4><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+    default: cov_tri_kernel<kPts, 0><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+  }
+}
+
 int construct(Ctx* ctx, int kind, const GenDev& g, const double* X, int64_t nx, const double* Y,
               int64_t ny, int b, double* out, cudaStream_t s) {
   const size_t smem = (size_t)b * (g.dim > 0 ? g.dim : 1) * sizeof(double);
   if (kind == BGP_TRI) {
     int T = (int)((nx + b - 1) / b);
     if (X)
-      cov_tri_kernel<true><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out, nullptr);
+      launch_cov_tri<true>(g, (unsigned)tri_count(T), smem, s, X, nx, T, b, out, nullptr);
     else
-      cov_tri_kernel<false><<<(unsigned)tri_count(T), kCovThreads, smem, s>>>(g, X, nx, T, b, out, nullptr);
+      launch_cov_tri<false>(g, (unsigned)tri_count(T), smem, s, X, nx, T, b, out, nullptr);
   } else if (kind == BGP_RECT) {
     int Tn = (int)((nx + b - 1) / b), Tm = (int)((ny + b - 1) / b);
     const unsigned grid = (unsigned)((int64_t)Tn * Tm);
@@ -195,9 +252,9 @@ int construct_tiles(Ctx* ctx, const GenDev& g, const double* X, int64_t n, int b
   const size_t smem = (size_t)b * (g.dim > 0 ? g.dim : 1) * sizeof(double);
   const int T = (int)((n + b - 1) / b);
   if (X)
-    cov_tri_kernel<true><<<(unsigned)count, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij);
+    launch_cov_tri<true>(g, (unsigned)count, smem, s, X, n, T, b, out, tile_ij);
   else
-    cov_tri_kernel<false><<<(unsigned)count, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij);
+    launch_cov_tri<false>(g, (unsigned)count, smem, s, X, n, T, b, out, tile_ij);
   ctx->launches++;
   return check_launch(ctx, "construct_tiles");
 }
