@@ -27,7 +27,7 @@ lib, ctx = cl.lib, cl._ctx
 lib.bgp_set_profiling(ctx, 1)
 prob.log_density(np.array([1.0, 0.08 + 1e-12, 0.02]))
 buf = (ctypes.c_double * 4096)()
-nst = lib.bgp_profile_steps(ctx, buf, 4096)
+nst = lib.bgp_profile_steps(ctx, buf, 4096) + 1  # + the re-tiled tail, if any
 b = args.tile
 T = (len(y) + b - 1) // b
 out = []
