@@ -31,6 +31,7 @@
 #include "panel_device.cuh"
 
 #include <stdio.h>
+#include <stdlib.h>
 
 // Compiled twice: here with the BK = 16 configuration (namespace bgp::bk16)
 // and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks per tile.
@@ -321,7 +322,11 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
   prefetch_tmap(tmB);
   prefetch_tmap(tmL);
   prefetch_tmap(tmC);
+#ifdef BGP_EXP_EVICT_NORMAL
+  const uint64_t pol_keep = l2_policy_evict_normal();
+#else
   const uint64_t pol_keep = l2_policy_evict_last();
+#endif
   const int kc_per_tile = p.b / BK;
   const int64_t ntasks = gemm_num_tasks(p);
   int stage = 0;
@@ -522,7 +527,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   // 0's producer is about to wait on a gate, so group 1 never waits on a
   // group that itself waits (the gated work may be group 1's own).
   bool stagger_arrive = (g == 0 && gwarp == 0);
+#ifndef BGP_EXP_NO_STAGGER
   if (g == 1) mbar_wait(stagger, 0);
+#endif
 #ifdef BGP_EXP_TRACE
   int t_idx = 0;
 #endif
@@ -768,10 +775,15 @@ void gemm_prepare() {
 }
 
 // 512 tiles: BK = 32 stages (half the barrier and TMA operations per DMMA);
-// smaller tiles keep BK = 16 (measured: C4 at b = 512 +0.9 %, b = 256 -1.7 %)
+// smaller tiles keep BK = 16 (measured: C4 at b = 512 +0.9 %, b = 256 -1.7 %).
+// BGP_GEMM_CFG=16 (diagnostics) forces the first configuration everywhere.
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
-  if (p.b >= 512) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
+  static const bool force16 = [] {
+    const char* e = getenv("BGP_GEMM_CFG");
+    return e && atoi(e) == 16;
+  }();
+  if (p.b >= 512 && !force16) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
   return bk16::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
 }
 #endif

@@ -11,6 +11,8 @@ if [ "$1" = "build" ]; then
       NO_TMA_NO_EPI) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       TRACE) F="-DBGP_EXP_TRACE";;
       BK32) F="-DBGP_GEMM_BK32";;
+      BK32_NOSTAG) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_STAGGER";;
+      BK32_EVN) F="-DBGP_GEMM_BK32 -DBGP_EXP_EVICT_NORMAL";;
       NO_BAR_TRACE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR -DBGP_EXP_TRACE";;
       NO_BAR) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR";;
     esac
