@@ -89,9 +89,9 @@ size_t tri_inv_smem_bytes();
 constexpr unsigned long long BGP_INFO_DATAFLOW_TIMEOUT = 1ull << 62;
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
                       const int* gate = nullptr, int gate_need = 0);
-// one_cta: the single-CTA block-diagonal variant (look-ahead stream, one free SM)
+// one-CTA block-diagonal inverse of a factored tile (panel_device.cuh)
 int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
-                   int* done = nullptr, bool one_cta = false);
+                   int* done = nullptr);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
                       int trans, cudaStream_t s, bool check_info = true);

@@ -268,7 +268,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   // tri_inv of K (needed when panel K has tiles below the diagonal)
   auto inverse = [&](int K) -> int {
     if (K + 1 >= T) return BGP_OK;
-    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, s, nullptr, true);
+    return launch_tri_inv(ctx, tiles + tri_index(K, K, T) * tsz, ctx->d_dinv, b, ctx->d_linv, s);
   };
   // standalone panel solve of K on the caller's stream
   auto panel_solve = [&](int K) -> int {
@@ -698,7 +698,7 @@ int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv, 
   const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, 0, ctx->d_dinv, s))) return rc;
-  if ((rc = launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s, nullptr, true))) return rc;
+  if ((rc = launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s))) return rc;
   return read_info(ctx, s, info);
 }
 
@@ -713,7 +713,7 @@ int bgp_tile_potrf_async(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0
   int rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s))) return rc;
-  if (linv) return launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s, nullptr, true);
+  if (linv) return launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s);
   return BGP_OK;
 }
 

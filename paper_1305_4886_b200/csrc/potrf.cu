@@ -1,21 +1,17 @@
-// K2a tile POTRF, K2b panel TRSM and the 32x32 diagonal-block inverses.
+// K2a tile POTRF and tile inverse kernels, the 32x32 diagonal-block
+// inverses of a factored triangle, and the FP64 substitution panel TRSM.
 //
 // Replaces the LAPACK calls inside the reference's block sweep:
 //   la.cholesky(A_JJ)                       bg/distla/kernels.py:146-148
 //   solve_triangular(L_JJ, A_IJ^T)^T        bg/distla/kernels.py:163-164
 // and the diagonal TRSM inside solve_rect (kernels.py:304-306).
 //
-// tile_potrf: one CTA factors a b x b diagonal tile held in global memory
-// (it is L2-resident: the trailing update just wrote it).  Right-looking with
-// 32-wide sub-panels: warp 0 factors the 32x32 diagonal block in registers
-// (lane = row, shuffles), warp 1 inverts it, all threads apply the inverse to
-// the sub-panel below, and the in-tile trailing update runs on FP64 DMMA with
-// both operands in shared memory.  The first non-positive (or NaN) pivot
-// records its 1-based global row in *info and stops the factorization.
-//
-// panel_trsm: X = A L^{-T} for a column of b x b tiles.  One CTA owns a
-// 32-row slab of one tile in shared memory and sweeps the 32-wide column
-// blocks: X_k = S_k Dinv_k^T, then S_{>k} -= X_k L_{>k,k}^T.
+// tile_potrf_kernel / tri_inv_diag_kernel wrap the device code in
+// panel_device.cuh (also run by the look-ahead CTA of the update launch).
+// The Cholesky's panel solve itself runs on the DMMA GEMM with the tile
+// inverse (gemm.cu); panel_trsm below (one CTA per 32-row slab of a tile,
+// X_k = S_k Dinv_k^T, then S_{>k} -= X_k L_{>k,k}^T) serves the kriging
+// multi-RHS solve and the multi-GPU tile API.
 #include "bgp_common.cuh"
 #include "bgp_internal.h"
 #include "panel_device.cuh"
@@ -58,62 +54,6 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   tile_potrf_device(A, b, row0, dinv, info, sm, tid, 0);
 }
 
-// Full inverse of a factored diagonal tile, Linv = L^{-1} (column-major b x b,
-// zero strict upper triangle), from its 32x32 diagonal-block inverses:
-//   Linv[i][j] = -Dinv_i * sum_{m=j}^{i-1} L[i][m] Linv[m][j]     (i > j)
-// One CTA per 32-wide column block j; it keeps its column of Linv blocks in
-// shared memory.  Feeds the panel TRSM on the DMMA GEMM (X = A Linv^T).
-__global__ void __launch_bounds__(256) tri_inv_kernel(const double* __restrict__ L,
-                                                      const double* __restrict__ dinv, int b,
-                                                      double* __restrict__ Linv, int* __restrict__ done) {
-  extern __shared__ double xs[];  // Linv blocks (i, j), i >= j: [(i-j)*32 + r]*33 + c
-  double* tmp = xs + (size_t)(b / NB) * NB * 33;  // 32 x 33
-  const int j = blockIdx.x, nbk = b / NB;
-  const int tid = threadIdx.x, r = tid & 31, c8 = tid >> 5;
-  for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
-    const int c = idx >> 5, rr = idx & 31;
-    xs[rr * 33 + c] = dinv[(int64_t)j * NB * NB + idx];
-  }
-  __syncthreads();
-  for (int i = j + 1; i < nbk; ++i) {
-    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int m = j; m < i; ++m) {
-      const double* Xm = xs + (size_t)(m - j) * NB * 33;
-#pragma unroll 8
-      for (int q = 0; q < NB; ++q) {
-        const double l = L[(int64_t)(m * NB + q) * b + i * NB + r];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) sacc[u] = fma(l, Xm[q * 33 + c8 + 8 * u], sacc[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) tmp[r * 33 + c8 + 8 * u] = sacc[u];
-    __syncthreads();
-    const double* Di = dinv + (int64_t)i * NB * NB;  // column-major: (r, q) at q*32 + r
-    double* Xi = xs + (size_t)(i - j) * NB * 33;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c8 + 8 * u;
-      double v = 0.0;
-#pragma unroll 8
-      for (int q = 0; q < NB; ++q) v = fma(Di[q * NB + r], tmp[q * 33 + c], v);
-      Xi[r * 33 + c] = -v;
-    }
-    __syncthreads();
-  }
-  // column block j of Linv: rows < 32j are zero
-  for (int idx = tid; idx < NB * b; idx += blockDim.x) {
-    const int c = idx / b, row = idx % b;
-    const int blk = row / NB;
-    const double v = (blk < j) ? 0.0 : xs[((size_t)(blk - j) * NB + (row & 31)) * 33 + c];
-    Linv[(int64_t)(j * NB + c) * b + row] = v;
-  }
-  if (done) {  // publish: the fused panel TRSM of the trailing update waits for all column blocks
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) atomicAdd(done, 1);
-  }
-}
 
 // Single-CTA inverse of a factored diagonal tile for the look-ahead stream
 // (where only one SM is free): Linv = L^{-1} by block diagonals.  Diagonal
@@ -247,7 +187,6 @@ void potrf_prepare() {
   if (!done) {
     cudaFuncSetAttribute(tile_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, diag_inv_kernel);
@@ -265,16 +204,10 @@ int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv,
 }
 
 int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
-                   int* done, bool one_cta) {
-  if (one_cta) {
-    tri_inv_diag_kernel<<<1, TINV_THREADS, tri_inv_smem_bytes(), s>>>(Ltile, dinv, b, Linv, done);
-    ctx->launches++;
-    return check_launch(ctx, "tri_inv_diag");
-  }
-  const size_t smem = ((size_t)(b / NB) * NB * 33 + NB * 33) * sizeof(double);
-  tri_inv_kernel<<<b / NB, 256, smem, s>>>(Ltile, dinv, b, Linv, done);
+                   int* done) {
+  tri_inv_diag_kernel<<<1, TINV_THREADS, tri_inv_smem_bytes(), s>>>(Ltile, dinv, b, Linv, done);
   ctx->launches++;
-  return check_launch(ctx, "tri_inv");
+  return check_launch(ctx, "tri_inv_diag");
 }
 
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s) {
