@@ -137,6 +137,7 @@ struct GemmProblem {
   double* dinv;
   double* linv;
   int diag_need;
+  double* cbase;       // set by launch_gemm: C tiles (register epilogue variant)
 };
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv = nullptr);

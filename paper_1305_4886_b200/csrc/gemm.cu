@@ -571,7 +571,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         phase ^= 1;
       }
       sb = (uint32_t)stage * STAGE_BYTES;
+#ifndef BGP_EXP_NO_STAGE_WAIT  // probe build (with NO_TMA): no per-stage wait
       mbar_wait(&gs.full[stage], phase);
+#endif
       load_frag<0>(f[0], offA[0][0] + sb, offA[1][0] + sb, offB[0][0] + sb, offB[1][0] + sb);
       mma_frag(acc, f[(HALVES - 1) & 1]);
       __syncwarp();
@@ -608,6 +610,33 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     }
     continue;
 #endif
+#ifdef BGP_EPI_RED
+    {
+      // straight from registers: red.global.add of -acc (updates) or plain
+      // stores (beta = 0 / TRSM) into the tile, no staging and no waits
+      double* ct = p.cbase + (int64_t)it.cTile * p.b * p.b;
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int m = it.mrow0 + wm * WM + i * 8 + q;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
+            if (it.lower && m < n) continue;  // strict upper triangle stays
+            double* a = ct + (int64_t)n * p.b + m;
+            if (it.store) *a = acc[i][j][e];
+            else asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(-acc[i][j][e]) : "memory");
+          }
+        }
+      }
+    }
+    if (it.gate >= 0) {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(p.col_gate + it.gate, 1);
+    }
+#else
 #pragma unroll
     for (int r = 0; r < EPI_ROUNDS; ++r) {
       if (lane == 0 && (store_pending || r > 0)) tma_store_wait_read0();  // slice free again
@@ -635,6 +664,8 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       }
     }
     store_pending = true;
+#endif
+#ifndef BGP_EPI_RED
     // Column-(J+1) gates: a warp signals a block once its bulk reduction has
     // retired (completion, proxy fence, release).  Not deferred: this group's
     // own producer may be the one waiting for the tile.
@@ -647,6 +678,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       }
       __syncwarp();
     }
+#endif
 #ifdef BGP_EXP_TRACE
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][2] = clock64();
@@ -728,6 +760,7 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
            const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
   if (p_in.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
   GemmProblem p = p_in;
+  p.cbase = Cbase;
   const int64_t tasks = gemm_num_tasks(p);
   if (tasks <= 0) return BGP_OK;
   int rc;

@@ -26,7 +26,7 @@ def _cov(n, seed):
     return np.exp(-d / 0.08) + 0.02 * np.eye(n)
 
 
-@pytest.mark.parametrize("tile,ntiles", [(128, 9), (256, 6), (512, 5)])
+@pytest.mark.parametrize("tile,ntiles", [(128, 9), (256, 6), (384, 6), (512, 5)])
 def test_lookahead_matches_lapack(cluster_factory, tile, ntiles):
     from paper_1305_4886_b200 import distla
     n = tile * ntiles - 37  # ragged last tile

@@ -11,6 +11,13 @@ if [ "$1" = "build" ]; then
       NO_TMA_NO_EPI) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       TRACE) F="-DBGP_EXP_TRACE";;
       BK32) F="-DBGP_GEMM_BK32";;
+      BK32_RED) F="-DBGP_GEMM_BK32 -DBGP_EPI_RED";;
+      BK32_RED_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EPI_RED -DBGP_EXP_TRACE";;
+      BK32_CORE) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
+      BK32_CORE_NW) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_STAGE_WAIT";;
+      BK16_CORE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
+      BK16_CORE_NW) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_STAGE_WAIT";;
+      BK32_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_TRACE";;
       BK32_NOSTAG) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_STAGGER";;
       BK32_EVN) F="-DBGP_GEMM_BK32 -DBGP_EXP_EVICT_NORMAL";;
       NO_BAR_TRACE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR -DBGP_EXP_TRACE";;
