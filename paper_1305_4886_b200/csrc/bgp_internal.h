@@ -81,6 +81,9 @@ int launch_tile_logdet(Ctx* ctx, const double* base, const int32_t* diag, int64_
 // loading must not happen while a look-ahead kernel spin-waits)
 void gemm_prepare();
 void potrf_prepare();
+// retire counts of the update launch's gates for tile size b (warp-blocks of
+// a full tile / of a diagonal tile) and consumer groups per CTA
+void gemm_block_counts(int b, int* tile_need, int* diag_need, int* groups_per_cta);
 size_t potrf_smem_bytes(int b);
 size_t tri_inv_smem_bytes();
 

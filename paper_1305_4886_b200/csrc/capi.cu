@@ -191,14 +191,6 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen, const doubl
   return construct(ctx, kind, g, X, nx, Y, ny, tile, out, (cudaStream_t)stream);
 }
 
-// number of 128x64 GEMM blocks of a diagonal tile (the rest lie strictly
-// above the diagonal and are skipped); gemm.cu diag_block
-static int diag_tile_blocks(int b) {
-  int c = 0;
-  for (int bi = 0; bi < b / 128; ++bi)
-    for (int bj = 0; bj < b / 64; ++bj) c += (bi * 128 + 127 >= bj * 64);
-  return c;
-}
 
 // Right-looking tile Cholesky with a one-panel look-ahead, one launch per
 // step.  The step-J trailing update is one persistent DMMA launch whose task
@@ -254,9 +246,8 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   }
   const int64_t ntiles = tri_count(T);
   const int64_t tsz = (int64_t)b * b;
-  const int nblk = (b / 128) * (b / 64);          // 128x64 blocks per tile (gemm.cu)
-  const int diag_need = diag_tile_blocks(b) * 4;  // 4 warps per block (gemm.cu GROUP_WARPS)
-  const int tile_need = nblk * 4;
+  int tile_need, diag_need, groups_per_cta;  // gate counts of the chosen GEMM configuration
+  gemm_block_counts(b, &tile_need, &diag_need, &groups_per_cta);
   // BGP_LOOKAHEAD (diagnostics): 1 (default) look-ahead inside the update
   // launch; 0 sequential launches on all SMs; 2 sequential with the update on
   // all SMs but one.  All look-ahead waits are inside one launch, so the
@@ -317,7 +308,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
         p.tile_need = tile_need;
         p.linv_flag = gate + T;
         p.linv_need = nbk;
-        p.trsm_tail = 12 * ctx->num_sms;  // ~6 update blocks per consumer group
+        p.trsm_tail = 6 * groups_per_cta * ctx->num_sms;  // ~6 update blocks per consumer group
         p.potrf_tile = dkk;
         p.potrf_row0 = row_base + (int64_t)K * b;
         p.dinv = ctx->d_dinv;

@@ -50,31 +50,40 @@ namespace BGP_GEMM_NS {
 // The two consumer groups take alternate blocks of the CTA's static schedule
 // and run concurrently, so one group's epilogue overlaps the other group's
 // main loop and the DMMA pipe never drains between blocks.
-#ifdef BGP_GEMM_BK32  // 2 stages of BK = 32, epilogue in 16-row rounds
+#if defined(BGP_GEMM_3G)  // three consumer groups of 2x2 warps of 32x32: 64x64 blocks
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 16;
+constexpr int GROUPS = 3;
+constexpr int WM = 32, WN = 32;                // warp tile
+constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 144;
+#elif defined(BGP_GEMM_BK32)  // 2 stages of BK = 32, epilogue in 16-row rounds
 constexpr int BM = 128, BN = 64, BK = 32, STAGES = 2, EPI_ROWS = 16;
+constexpr int GROUPS = 2;
+constexpr int WM = 64, WN = 32;
+constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
 #else
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 32;
-#endif
 constexpr int GROUPS = 2;
+constexpr int WM = 64, WN = 32;
+constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
+#endif
 constexpr int WARPS_M = 2, WARPS_N = 2;       // per consumer group
 constexpr int GROUP_WARPS = WARPS_M * WARPS_N;
 constexpr int THREADS = 128 * (GROUPS + 1);
-constexpr int WM = 64, WN = 32;                // warp tile
 constexpr int MI = WM / 8, NJ = WN / 8;        // 8x8 DMMA tiles per warp
+static_assert(BM == WARPS_M * WM && BN == WARPS_N * WN, "block = 2 x 2 warp tiles");
 constexpr int BOX_BYTES = 16 * BK * 8;         // 2 KB: operand TMA box of 16 rows x BK k
 constexpr int STAGE_A_BYTES = BM * BK * 8;     // 16 KB: 8 boxes
 constexpr int STAGE_B_BYTES = BN * BK * 8;     // 8 KB: 4 boxes
 constexpr int STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr int WBOX_BYTES = 16 * WN * 8;        // 4 KB: epilogue box of 16 rows x 32 cols
 constexpr int EPI_BOXES = EPI_ROWS / 16;       // boxes per epilogue round
-constexpr int EPI_ROUNDS = 64 / EPI_ROWS;      // rounds per 64-row warp tile
+constexpr int EPI_ROUNDS = WM / EPI_ROWS;      // rounds per warp tile
 constexpr int WSTAGE_BYTES = EPI_BOXES * WBOX_BYTES;  // a warp's epilogue slice (one round)
 constexpr int HALVES = BK / 4;                 // k4 half-steps per stage
 constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
-constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 #ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
@@ -409,10 +418,12 @@ __device__ __forceinline__ void load_frag(Frag& f, uint32_t a0, uint32_t a1, uin
   f.a[1] = lds64<K>(a1);
   f.a[2] = lds64<K + BOX_BYTES>(a0);
   f.a[3] = lds64<K + BOX_BYTES>(a1);
-  f.a[4] = lds64<K + 2 * BOX_BYTES>(a0);
-  f.a[5] = lds64<K + 2 * BOX_BYTES>(a1);
-  f.a[6] = lds64<K + 3 * BOX_BYTES>(a0);
-  f.a[7] = lds64<K + 3 * BOX_BYTES>(a1);
+  if constexpr (MI == 8) {
+    f.a[4] = lds64<K + 2 * BOX_BYTES>(a0);
+    f.a[5] = lds64<K + 2 * BOX_BYTES>(a1);
+    f.a[6] = lds64<K + 3 * BOX_BYTES>(a0);
+    f.a[7] = lds64<K + 3 * BOX_BYTES>(a1);
+  }
   f.b[0] = lds64<K>(b0);
   f.b[1] = lds64<K>(b1);
   f.b[2] = lds64<K + BOX_BYTES>(b0);
@@ -496,7 +507,7 @@ __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ]
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p,
                                               uint64_t* stagger) {
-  static_assert(MI == 8 && NJ == 4 && WM / 16 == 4 && WN / 16 == 2, "load_frag assumes a 64x32 warp tile");
+  static_assert((MI == 8 || MI == 4) && NJ == 4 && WN / 16 == 2, "load_frag: 64x32 or 32x32 warp tiles");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
   const int kc_per_tile = p.b / BK;
@@ -723,18 +734,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     if (lookahead_cta) {
-      // the 256 consumer threads run the tile POTRF (and inverse) on the ring
-      // memory once the update blocks of the diagonal tile retired; other
-      // CTAs' TRSM tasks wait for the published inverse
+      // the first 256 consumer threads run the tile POTRF (and inverse) on
+      // the ring memory once the update blocks of the diagonal tile retired;
+      // other CTAs' TRSM tasks wait for the published inverse
       const int ctid = threadIdx.x - 128;
-      double* psm = reinterpret_cast<double*>(smem);
-      if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
-      named_bar_sync(2, 256);
-      if (s_go && tile_potrf_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info, psm, ctid, 2) && p.trsm_next) {
-        tri_inv_diag_device(p.potrf_tile, p.dinv, p.b, p.linv, psm, ctid, 2);
-        __threadfence();
+      if (ctid < 256) {
+        double* psm = reinterpret_cast<double*>(smem);
+        if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
         named_bar_sync(2, 256);
-        if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);
+        if (s_go && tile_potrf_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info, psm, ctid, 2) &&
+            p.trsm_next) {
+          tri_inv_diag_device(p.potrf_tile, p.dinv, p.b, p.linv, psm, ctid, 2);
+          __threadfence();
+          named_bar_sync(2, 256);
+          if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);
+        }
       }
       named_bar_sync(1, THREADS);  // release this CTA's producers
     }
@@ -746,6 +760,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 // One-time function setup.  It also forces the module to load: with CUDA's
 // lazy loading, the first launch of a kernel while a spin-waiting kernel runs
 // on another stream (the look-ahead POTRF) could otherwise stall behind it.
+// blocks of one b x b tile, and of a diagonal tile (the rest lie strictly
+// above the diagonal), for the host's gate counts; warps per block
+int tile_blocks(int b) { return (b / BM) * (b / BN); }
+int diag_blocks(int b) {
+  int c = 0;
+  for (int bi = 0; bi < b / BM; ++bi)
+    for (int bj = 0; bj < b / BN; ++bj) c += (bi * BM + BM - 1 >= bj * BN);
+  return c;
+}
+int block_warps() { return GROUP_WARPS; }
+int groups() { return GROUPS; }
+
 void prepare() {
   static int occupancy = -1;
   if (occupancy < 0) {
@@ -800,7 +826,31 @@ namespace bk32 {
 void prepare();
 int launch(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA, const double* Bbase,
            int64_t nB, int64_t nC, cudaStream_t s, const double* Linv);
+int tile_blocks(int b);
+int diag_blocks(int b);
+int block_warps();
+int groups();
 }  // namespace bk32
+
+static bool use_bk32(int b) {
+  static const bool force16 = [] {
+    const char* e = getenv("BGP_GEMM_CFG");
+    return e && atoi(e) == 16;
+  }();
+  return b >= 512 && !force16;
+}
+
+void gemm_block_counts(int b, int* tile_need, int* diag_need, int* groups_per_cta) {
+  if (use_bk32(b)) {
+    *tile_need = bk32::tile_blocks(b) * bk32::block_warps();
+    *diag_need = bk32::diag_blocks(b) * bk32::block_warps();
+    *groups_per_cta = bk32::groups();
+  } else {
+    *tile_need = bk16::tile_blocks(b) * bk16::block_warps();
+    *diag_need = bk16::diag_blocks(b) * bk16::block_warps();
+    *groups_per_cta = bk16::groups();
+  }
+}
 
 void gemm_prepare() {
   bk16::prepare();
@@ -812,11 +862,7 @@ void gemm_prepare() {
 // BGP_GEMM_CFG=16 (diagnostics) forces the first configuration everywhere.
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
-  static const bool force16 = [] {
-    const char* e = getenv("BGP_GEMM_CFG");
-    return e && atoi(e) == 16;
-  }();
-  if (p.b >= 512 && !force16) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
+  if (use_bk32(p.b)) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
   return bk16::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
 }
 #endif

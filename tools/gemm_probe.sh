@@ -17,6 +17,8 @@ if [ "$1" = "build" ]; then
       BK32_CORE_NW) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_STAGE_WAIT";;
       BK16_CORE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       BK16_CORE_NW) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_STAGE_WAIT";;
+      G3) F="-DBGP_GEMM_3G";;
+      G3_CORE) F="-DBGP_GEMM_3G -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       BK32_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_TRACE";;
       BK32_NOSTAG) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_STAGGER";;
       BK32_EVN) F="-DBGP_GEMM_BK32 -DBGP_EXP_EVICT_NORMAL";;
