@@ -14,6 +14,8 @@
 #include "bgp_common.cuh"
 #include "bgp_internal.h"
 
+#include <cmath>
+
 namespace bgp {
 
 constexpr int kMaxDim = 4;
@@ -88,16 +90,38 @@ __device__ __forceinline__ double div_rho(double x, double rho, double rinv) {
   return fma(fma(-q, rho, x), rinv, q);
 }
 
+// exp(x) for x <= 0 by table: x log2(e) = n + j/64 + f, |f| <= 1/128, so
+// exp(x) = 2^n * 2^(j/64) * exp(r), |r| <= ln2/128, with a degree-6
+// polynomial (truncation < 1e-18): within ~1 ulp of exp, about half the
+// FP64 instructions of the library exp.  Underflow (x < -708) -> 0.
+__device__ double kExp2Tab[64];  // 2^(j/64); read through L1 (__ldg): indices diverge across a warp
+__device__ __forceinline__ double exp_neg(double x) {
+  if (x < -708.0) return 0.0;
+  const double kd = rint(x * 92.33248261689366);  // 64 / ln 2
+  const int k = (int)kd;
+  double r = fma(kd, -0.010830424696249145, x);  // Cody-Waite: ln2/64 = hi + lo
+  r = fma(kd, -3.623510646634843e-19, r);
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(r, p, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = fma(r, p, 1.0);
+  const int n = k >> 6, j = k & 63;  // k <= 0: arithmetic shift floors
+  const double v = __ldg(&kExp2Tab[j]) * p;
+  return __hiloint2double(__double2hiint(v) + (n << 20), __double2loint(v));
+}
+
 template <int KIND>
 __device__ __forceinline__ double corr2d(double dx, double dy, const GenDev& g, double rinv) {
   const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
   if (KIND == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 * (d/rho)**2)
     const double t = div_rho(dist, g.p[1], rinv);
-    return exp(__dmul_rn(-0.5, __dmul_rn(t, t)));
+    return exp_neg(__dmul_rn(-0.5, __dmul_rn(t, t)));
   }
   // bg/gp/kernels.py:16-29: s = sqrt(2 nu) * d / rho
   const double sv = div_rho(__dmul_rn(g.sqrt2nu, dist), g.p[1], rinv);
-  const double e = exp(-sv);
+  const double e = exp_neg(-sv);
   if (KIND == 1) return e;
   if (KIND == 2) return __dmul_rn(__dadd_rn(1.0, sv), e);
   return __dmul_rn(__dadd_rn(__dadd_rn(1.0, sv), __ddiv_rn(__dmul_rn(sv, sv), 3.0)), e);
@@ -210,9 +234,19 @@ static int cov_kind(const GenDev& g) {
   return 0;
 }
 
+static void init_exp_table() {
+  static bool done = false;
+  if (done) return;
+  double tab[64];
+  for (int j = 0; j < 64; ++j) tab[j] = (double)exp2l((long double)j / 64.0L);
+  cudaMemcpyToSymbol(kExp2Tab, tab, sizeof(tab));
+  done = true;
+}
+
 template <bool kPts>
 static void launch_cov_tri(const GenDev& g, unsigned grid, size_t smem, cudaStream_t s, const double* X, int64_t n,
                            int T, int b, double* out, const int32_t* tile_ij) {
+  init_exp_table();
   switch (kPts ? cov_kind(g) : 0) {
     case 1: cov_tri_kernel<kPts, 1><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
     case 2: cov_tri_kernel<kPts, 2><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
