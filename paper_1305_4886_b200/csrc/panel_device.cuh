@@ -127,6 +127,47 @@ __device__ __forceinline__ void tile_trailing(double* A, int b, int base_rc, con
   }
 }
 
+// One 32x32 block (bi, bj), bi >= bj, of the in-tile trailing update
+// A[i][j] -= sum_k P[i][k] P[j][k] (rows/cols relative to base_rc): all 32
+// C values of a lane load at once (one L2 round trip per block instead of
+// one per 8x8), then 8 k4-steps of 16 DMMAs with fragments from P in smem.
+__device__ __forceinline__ void trail_block32(double* A, int b, int base_rc, const double* P, int bi, int bj,
+                                              int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = bi * 32 + tr * 8 + q, n = bj * 32 + tc * 8 + 2 * s4 + e;
+        acc[tr][tc][e] = A[(int64_t)(base_rc + n) * b + base_rc + m];
+      }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      av[t] = -P[(bi * 32 + t * 8 + q) * PLD + 4 * k + s4];
+      bv[t] = P[(bj * 32 + t * 8 + q) * PLD + 4 * k + s4];
+    }
+#pragma unroll
+    for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+      for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[tr], bv[tc]);
+  }
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = bi * 32 + tr * 8 + q, n = bj * 32 + tc * 8 + 2 * s4 + e;
+        if (bi != bj || m >= n) A[(int64_t)(base_rc + n) * b + base_rc + m] = acc[tr][tc][e];
+      }
+}
+
 // Right-looking blocked factorization of one b x b tile with 32-wide
 // sub-panels and a one-block look-ahead inside the tile: while warps 1..7
 // apply sub-panel k's trailing update, warp 0 updates, factors and inverts
@@ -164,34 +205,50 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
   for (int kb = 0; kb + 1 < nbk; ++kb) {
     const int c0 = kb * NB;
     const int rest = b - c0 - NB;
-    // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy);
-    // Dinv is lower triangular with explicit zeros, so every dot is 32 long
-    for (int r = tid; r < rest; r += POTRF_THREADS) {
-      const int64_t gi = c0 + NB + r;
-      double av[NB];
+    // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy),
+    // one 32-row block per warp on DMMA: the lane's 32 A values load at once
+    // (one L2 round trip), Dinv (lower triangular, explicit zeros) from smem
+    for (int t = warp; t < rest / NB; t += POTRF_THREADS / 32) {
+      const int q = lane >> 2, s4 = lane & 3;
+      const int r0 = t * NB;  // rows c0 + 32 + r0 .. of the tile
+      double av[4][8];
 #pragma unroll
-      for (int k = 0; k < NB; ++k) av[k] = A[(int64_t)(c0 + k) * b + gi];
-#pragma unroll 2
-      for (int j = 0; j < NB; ++j) {
-        const double* dj = Dinv_s + j * 33;
-        double s0 = 0.0, s1 = 0.0;
+      for (int tr = 0; tr < 4; ++tr)
 #pragma unroll
-        for (int k = 0; k < NB; k += 2) {
-          s0 = fma(av[k], dj[k], s0);
-          s1 = fma(av[k + 1], dj[k + 1], s1);
-        }
-        const double x = s0 + s1;
-        A[(int64_t)(c0 + j) * b + gi] = x;
-        P[r * PLD + j] = x;
+        for (int kk = 0; kk < 8; ++kk) av[tr][kk] = A[(int64_t)(c0 + 4 * kk + s4) * b + c0 + NB + r0 + tr * 8 + q];
+      double acc[4][4][2];
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        double bv[4];
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) bv[tc] = Dinv_s[(tc * 8 + q) * 33 + 4 * kk + s4];
+#pragma unroll
+        for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+          for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[tr][kk], bv[tc]);
       }
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = r0 + tr * 8 + q, j = tc * 8 + 2 * s4 + e;
+            A[(int64_t)(c0 + j) * b + c0 + NB + r] = acc[tr][tc][e];
+            P[r * PLD + j] = acc[tr][tc][e];
+          }
     }
     named_bar_sync(bar, POTRF_THREADS);
-    // (B) trailing update; the first 10 blocks are diagonal block k+1
-    const int nb8 = rest / 8;
-    const int nblk = nb8 * (nb8 + 1) / 2;
+    // (B) trailing update in 32x32 blocks; block (0, 0) is diagonal block k+1
+    const int nb32 = rest / 32;
+    const int nblk = nb32 * (nb32 + 1) / 2;
     const int base_rc = c0 + NB;
     if (warp == 0) {
-      tile_trailing(A, b, base_rc, P, 0, 10, 0, 1, lane);
+      trail_block32(A, b, base_rc, P, 0, 0, lane);
       __syncwarp();
       __threadfence_block();
       const unsigned fm = warp_potrf32(A, b, base_rc, D, rdiag, col, lane);
@@ -204,7 +261,12 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
         warp_trinv32(D, rdiag, Dinv_s, dinv ? dinv + (int64_t)(kb + 1) * NB * NB : nullptr, lane);
       }
     } else {
-      tile_trailing(A, b, base_rc, P, 10, nblk, warp - 1, POTRF_THREADS / 32 - 1, lane);
+      for (int t = warp; t < nblk; t += POTRF_THREADS / 32 - 1) {  // blocks 1.., row-major lower
+        int bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+        while (bi * (bi + 1) / 2 > t) --bi;
+        trail_block32(A, b, base_rc, P, bi, t - bi * (bi + 1) / 2, lane);
+      }
     }
     named_bar_sync(bar, POTRF_THREADS);
     if (*s_fail) return false;
