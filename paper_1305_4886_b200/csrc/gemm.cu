@@ -203,7 +203,11 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   it.lower = 0;
   it.bTriRow = -1;
   it.kstages = 0;
+#ifdef BGP_EXP_STORE_EPI  // probe build: updates stored instead of reduced (wrong results; timing only)
+  it.store = 1;
+#else
   it.store = (p.beta == 0.0);
+#endif
   it.bLinv = 0;
   it.gate = -1;
   int64_t idx;
