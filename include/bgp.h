@@ -246,6 +246,11 @@ int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count,
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
                     const double* Bbase, const int32_t* triples /*device, 4 per*/,
                     int64_t count, int tile, void* stream);
+/* bgp_tile_update on at most max_ctas CTAs (leaves SMs to concurrent work
+ * such as NCCL collectives on another stream). */
+int bgp_tile_update_limited(bgp_ctx_t ctx, double* Cbase, const double* Abase,
+                            const double* Bbase, const int32_t* triples, int64_t count,
+                            int tile, int max_ctas, void* stream);
 
 /* ---- measurement ----------------------------------------------------------
  * When profiling is on, bgp_potrf brackets every launch with CUDA events

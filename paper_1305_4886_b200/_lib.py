@@ -73,6 +73,7 @@ SIGNATURES = {
     "bgp_panel_trsm_inv": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
+    "bgp_tile_update_limited": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _int, _c_dp]),
     "bgp_construct_tiles": (_int, [ctypes.c_void_p, ctypes.POINTER(Generator), _c_dp, _i64, _int, _int,
                                    _c_dp, _i64, _c_dp, _c_dp]),
     "bgp_tile_trsv": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, _i64, _c_dp, _int,

@@ -736,6 +736,23 @@ int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, in
   return launch_panel_trsm(ctx, Ld, ctx->d_dinv, A, count, tile, 0, s, false);
 }
 
+int bgp_tile_update_limited(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase,
+                            const int32_t* triples, int64_t count, int tile, int max_ctas, void* stream) {
+  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
+  if (count == 0) return BGP_OK;
+  GemmProblem p{};
+  p.mode = GEMM_LIST;
+  p.b = tile;
+  p.count = count;
+  p.items = triples;
+  p.alpha = -1.0;
+  p.beta = 1.0;
+  p.check_info = false;
+  p.grid_limit = max_ctas > 0 ? max_ctas : 0;
+  const int64_t big = (int64_t)1 << 30;
+  return launch_gemm(ctx, p, Cbase, Abase, big, Bbase, big, big, (cudaStream_t)stream);
+}
+
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase, const int32_t* triples,
                     int64_t count, int tile, void* stream) {
   if (!valid_tile(tile) || count < 0) return BGP_E_ARG;

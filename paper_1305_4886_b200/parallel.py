@@ -123,49 +123,72 @@ class TileDist:
 
 
 def dist_cholesky(dist, local, ops, comm):
-    """Right-looking tiled Cholesky of a distributed matrix, in place.
+    """Right-looking tiled Cholesky of a distributed matrix, in place, with a
+    one-panel look-ahead.
 
     `local` is this rank's (count, b, b) tile stack.  Returns the first
     failing pivot row (1-based, LAPACK info) agreed by all ranks, or 0.
 
-    Per step J the owner of (J, J) factors it and inverts it; the inverse is
-    broadcast and the ranks of process column J mod Pc solve their panel tiles
-    as A <- A Linv^T (the DMMA GEMM on the GPU).  The update items of every
-    step are built and uploaded once, and pivot failures stay in the device
-    status until the end, so the host never waits on the GPU inside the loop.
+    Step J: every rank first updates its tiles of column J+1 with panel J.
+    Then, on the side stream (ops.side()), the owner of (J+1, J+1) factors
+    and inverts it, the inverse is broadcast, process column (J+1) mod Pc
+    solves its panel tiles (A <- A Linv^T on the DMMA GEMM) and the panel is
+    broadcast row chunk by row chunk -- while the rest of the trailing update
+    (columns >= J+2, panel J) runs on the compute stream on all SMs but a few
+    (ops.update(..., reserve=True)), which the collectives and the small
+    panel kernels use.  ops.join_side() then orders step J+1 after panel J+1.
+    The update items of every step are built and uploaded once, and a failing
+    pivot stays in the device status until the end, so the host never waits
+    on the GPU inside the loop.
     """
     b, T, me = dist.b, dist.T, dist.rank
     inv_buf = ops.empty((b, b))
     ops.begin()
-    info = 0
-    panel = None
+    info = [0]
+    panels = [None, None]
     layouts = [dist.panel_layout(J) for J in range(T - 1)]
-    items = ops.prepare_items([dist.update_items(J, layouts[J][1]) for J in range(T - 1)])
-    for J in range(T):
-        d = dist.owner(J, J)
+    col_items, rest_items = [], []
+    for J in range(T - 1):
+        it = np.asarray(dist.update_items(J, layouts[J][1])).reshape(-1, 4)
+        cols = dist.tiles[it[:, 0], 1] if len(it) else np.zeros(0, dtype=np.int32)
+        col_items.append(it[cols == J + 1])
+        rest_items.append(it[cols != J + 1])
+    dev_col = ops.prepare_items(col_items)
+    dev_rest = ops.prepare_items(rest_items)
+
+    def factor_panel(K):
+        d = dist.owner(K, K)
         if me == d:
-            info = info or ops.potrf_factor(local, dist.local[(J, J)], J * b, inv_buf if J + 1 < T else None)
-        if J + 1 >= T:
-            break
+            info[0] = info[0] or ops.potrf_factor(local, dist.local[(K, K)], K * b,
+                                                  inv_buf if K + 1 < T else None)
+        if K + 1 >= T:
+            return
         comm.broadcast(inv_buf, d)
-        s, c = dist.my_panel(J)
+        s, c = dist.my_panel(K)
         if c:
             ops.trsm_inv(inv_buf, local, s, c)
-        chunks, slot, ntot = layouts[J]
-        if panel is None or panel.shape[0] < ntot:
-            panel = ops.empty((max(ntot, 1), b, b))
+        chunks, _, ntot = layouts[K]
+        if panels[K % 2] is None or panels[K % 2].shape[0] < ntot:
+            panels[K % 2] = ops.empty((max(ntot, 1), b, b))
+        panel = panels[K % 2]
         for root, off, cnt in chunks:
             if cnt == 0:
                 continue
             view = panel[off:off + cnt]
             if me == root:
-                ps, pcount = dist.my_panel(J)
+                ps, pcount = dist.my_panel(K)
                 assert pcount == cnt
                 ops.copy_tiles(view, local, ps, cnt)
             comm.broadcast(view, root)
-        ops.update(local, panel, items[J])
-    info = ops.end(info)
-    return comm.min_nonzero(info)
+
+    factor_panel(0)
+    for J in range(T - 1):
+        ops.update(local, panels[J % 2], dev_col[J])
+        with ops.side():
+            factor_panel(J + 1)
+        ops.update(local, panels[J % 2], dev_rest[J], reserve=True)
+        ops.join_side()
+    return comm.min_nonzero(ops.end(info[0]))
 
 
 def dist_trsv(dist, local, y, ops, comm, forward=True):
@@ -316,15 +339,36 @@ class LibTileOps:
             off += len(a)
         return out
 
-    def update(self, local, panel, items):
+    # SMs left free during a reserved update for the side stream's NCCL
+    # collectives, POTRF and panel solve
+    RESERVE_SMS = 8
+
+    def side(self):
+        """Context: run on the side stream, after the work enqueued so far."""
+        import torch
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.cl.device)
+        self._side.wait_stream(torch.cuda.current_stream(self.cl.device))
+        return torch.cuda.stream(self._side)
+
+    def join_side(self):
+        import torch
+        if getattr(self, "_side", None) is not None:
+            torch.cuda.current_stream(self.cl.device).wait_stream(self._side)
+
+    def update(self, local, panel, items, reserve=False):
         if isinstance(items, tuple):
             dev, count = items
         else:
             dev, count = self._items(items), len(items)
         if count == 0:
             return
-        self.cl.call("bgp_tile_update", self._p(local), self._p(panel), self._p(panel),
-                     self._p(dev), count, self.b, self.cl.stream)
+        if reserve:
+            self.cl.call("bgp_tile_update_limited", self._p(local), self._p(panel), self._p(panel),
+                         self._p(dev), count, self.b, self.cl.num_sms - self.RESERVE_SMS, self.cl.stream)
+        else:
+            self.cl.call("bgp_tile_update", self._p(local), self._p(panel), self._p(panel),
+                         self._p(dev), count, self.b, self.cl.stream)
 
     def sub_into(self, out, a, b):
         self.cl.call("bgp_sub", self._p(a), self._p(b), self._p(out), out.numel(), self.cl.stream)

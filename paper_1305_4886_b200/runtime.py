@@ -99,6 +99,10 @@ class B200Cluster:
     def stream(self):
         return _torch().cuda.current_stream(self.device).cuda_stream
 
+    @property
+    def num_sms(self):
+        return _torch().cuda.get_device_properties(self.device).multi_processor_count
+
     def call(self, name, *args):
         """Invoke a libbgp entry point; non-zero status -> WorkerFailure."""
         rc = getattr(self.lib, name)(self._ctx, *args)

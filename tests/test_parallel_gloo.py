@@ -79,7 +79,14 @@ class NumpyTileOps:
             M = self._m(local[t])
             M[:] = la.solve_triangular(L, M.T, lower=True).T
 
-    def update(self, local, panel, items):
+    def side(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def join_side(self):
+        pass
+
+    def update(self, local, panel, items, reserve=False):
         for c, a, b, lower in items:
             M = self._m(local[c])
             U = self._m(panel[a]) @ self._m(panel[b]).T
