@@ -733,7 +733,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (lookahead_cta) named_bar_sync(1, THREADS);  // wait for the panel work below
+#ifdef BGP_EXP_ONE_GROUP  // probe build: only consumer group 0 works (single-warp-per-SMSP rate)
+    if (warp < 1 && lane == 0)
+#else
     if (warp < GROUPS && lane == 0)
+#endif
       producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmC, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
@@ -757,6 +761,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       named_bar_sync(1, THREADS);  // release this CTA's producers
     }
     const int g = wg - 1;
+#ifdef BGP_EXP_ONE_GROUP
+    if (g != 0) return;
+#endif
     consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem));
   }
 }

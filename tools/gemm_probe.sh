@@ -18,6 +18,8 @@ if [ "$1" = "build" ]; then
       BK16_CORE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       BK16_CORE_NW) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_STAGE_WAIT";;
       BK32_STORE) F="-DBGP_GEMM_BK32 -DBGP_EXP_STORE_EPI";;
+      BK32_ONE) F="-DBGP_GEMM_BK32 -DBGP_EXP_ONE_GROUP";;
+      BK32_ONE_CORE) F="-DBGP_GEMM_BK32 -DBGP_EXP_ONE_GROUP -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       G3) F="-DBGP_GEMM_3G";;
       G3_CORE) F="-DBGP_GEMM_3G -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       BK32_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_TRACE";;
