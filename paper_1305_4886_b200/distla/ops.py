@@ -54,18 +54,78 @@ def _packed_index(dist):
     return torch.from_numpy(J * T - J * (J - 1) // 2 + (I - J))
 
 
+def _rank_maps(ctx, n):
+    """(count, packed index on the device) of every rank's tiles, cached per n."""
+    cache = ctx.__dict__.setdefault("_rank_tile_maps", {})
+    key = (n, ctx.tile)
+    if key not in cache:
+        from ..parallel import TileDist
+        maps = []
+        for r in range(ctx.G):
+            td = TileDist(n, ctx.tile, ctx.grid, r)
+            maps.append((td.count, _packed_index(td).to(ctx.device)))
+        cache[key] = maps
+    return cache[key]
+
+
 def _full(ctx, obj):
     """Replicated packed copy of a distributed triangular object (for the
     operations that run on one GPU's full copy: collect, kriging solves,
-    crossproducts, elementwise helpers)."""
+    crossproducts, elementwise helpers): one all-gather of every rank's
+    tiles (padded to the largest share), scattered to packed order."""
     if obj.dist is None:
         return obj
     d = obj.dist
-    full = ctx.zeros((d.T * (d.T + 1) // 2, obj.tile, obj.tile))
+    maps = _rank_maps(ctx, obj.n)
+    width = max(c for c, _ in maps)
+    part = ctx.empty((max(width, 1), obj.tile, obj.tile))
     if d.count:
-        full.index_copy_(0, _packed_index(d).to(full.device), obj.data[:d.count])
-    ctx.comm.all_reduce_sum(full)
+        part[:d.count].copy_(obj.data[:d.count])
+    full = ctx.empty((d.T * (d.T + 1) // 2, obj.tile, obj.tile))
+    for (count, idx), piece in zip(maps, ctx.comm.all_gather(part)):
+        if count:
+            full.index_copy_(0, idx, piece[:count])
     return DevObj(obj.kind, obj.row_layout, obj.col_layout, obj.tile, full)
+
+
+def _my_cols(ctx, m):
+    """Column shards of an m-column object over the job's GPUs (tile rows of
+    the transposed storage) and this rank's (r0, r1)."""
+    from ..parallel import col_shards
+    shards = col_shards(_ntiles(m, ctx.tile), ctx.G)
+    return shards, shards[ctx.rank - 1]
+
+
+def _gather_rect(ctx, X, Tn, Tm, shards):
+    """All-gather column shards (Tn, r1 - r0, b, b) into a replicated
+    (Tn * Tm, b, b) transposed rectangular object."""
+    from ..parallel import gather_col_shards
+    b = ctx.tile
+    width = max(r1 - r0 for r0, r1 in shards)
+    part = ctx.zeros((Tn, width, b, b))
+    part[:, :X.shape[1]].copy_(X)
+    full = ctx.empty((Tn * Tm, b, b))
+    view = full.view(Tn, Tm, b, b)
+
+    def fill(r0, r1, piece):
+        view[:, r0:r1].copy_(piece)
+    gather_col_shards(ctx.comm, part, shards, fill)
+    return full
+
+
+def _gather_vec(ctx, w, shards):
+    """All-gather per-rank m-vector shards (tile rows r0..r1) into one vector."""
+    from ..parallel import gather_col_shards
+    b = ctx.tile
+    width = max(r1 - r0 for r0, r1 in shards)
+    part = ctx.zeros((1, width * b))
+    part[0, :w.shape[0]].copy_(w)
+    full = ctx.zeros((shards[-1][1] * b,))
+
+    def fill(r0, r1, piece):
+        full[r0 * b:r1 * b].copy_(piece.reshape(-1)[:(r1 - r0) * b])
+    gather_col_shards(ctx.comm, part.view(1, width, b), shards, fill)
+    return full
 
 
 def _tile_ops(ctx, n):
@@ -251,10 +311,26 @@ def solve_rect(ctx, l_name, rhs_name, out_name, forward=True):
     B = _need(ctx, rhs_name, "rectangular")
     if B.n != L.n:
         raise DimensionMismatch("rhs rows do not conform to L")
-    X = B.data.clone()
     info = ctypes.c_int64(0)
-    ctx.call("bgp_trsm_rect", _ptr(L.data), L.n, L.tile, _ptr(X), B.m, 0 if forward else 1,
-             ctypes.byref(info), ctx.stream)
+    if ctx.G > 1:
+        # columns are independent: each GPU solves its shard of the RHS
+        # columns against the replicated L, then the shards are all-gathered
+        #
+        b = ctx.tile
+        Tm, Tn = _ntiles(B.m, b), _ntiles(B.n, b)
+        shards, (r0, r1) = _my_cols(ctx, B.m)
+        X = B.data.view(Tn, Tm, b, b)[:, r0:r1].contiguous()
+        mloc = max(0, min(B.m, r1 * b) - r0 * b)
+        if mloc:
+            ctx.call("bgp_trsm_rect", _ptr(L.data), L.n, L.tile, _ptr(X), mloc, 0 if forward else 1,
+                     ctypes.byref(info), ctx.stream)
+        info.value = ctx.comm.min_nonzero(info.value)
+        if not info.value:
+            X = _gather_rect(ctx, X, Tn, Tm, shards)
+    else:
+        X = B.data.clone()
+        ctx.call("bgp_trsm_rect", _ptr(L.data), L.n, L.tile, _ptr(X), B.m, 0 if forward else 1,
+                 ctypes.byref(info), ctx.stream)
     if info.value:
         raise SingularDiagonal(f"zero diagonal at row {info.value}")
     ctx.store[out_name] = DevObj("rectangular", B.row_layout, B.col_layout, B.tile, X)
@@ -270,9 +346,28 @@ def xprod_mat_vec(ctx, v_name, u_name, out_name):
     u = _need(ctx, u_name, "vector")
     if u.n != V.n:
         raise DimensionMismatch("u does not conform to V")
-    w = _alloc(ctx, "vector", V.m)
-    ctx.call("bgp_xprod_mat_vec", _ptr(V.data), V.n, V.m, V.tile, _ptr(u.data), _ptr(w), ctx.stream)
+    if ctx.G > 1:
+        w = _sharded_cols(ctx, V, lambda Vs, mloc, ws: ctx.call(
+            "bgp_xprod_mat_vec", _ptr(Vs), V.n, mloc, V.tile, _ptr(u.data), _ptr(ws), ctx.stream))
+    else:
+        w = _alloc(ctx, "vector", V.m)
+        ctx.call("bgp_xprod_mat_vec", _ptr(V.data), V.n, V.m, V.tile, _ptr(u.data), _ptr(w), ctx.stream)
     ctx.store[out_name] = DevObj("vector", V.col_layout, None, V.tile, w)
+
+
+def _sharded_cols(ctx, V, kernel):
+    """Per-column reduction of a replicated rectangular V on G > 1 GPUs: each
+    rank runs `kernel(V shard, local columns, out shard)` on its column shard
+    and the m-vector shards are all-gathered in rank order."""
+    b = ctx.tile
+    Tm, Tn = _ntiles(V.m, b), _ntiles(V.n, b)
+    shards, (r0, r1) = _my_cols(ctx, V.m)
+    mloc = max(0, min(V.m, r1 * b) - r0 * b)
+    ws = ctx.zeros(((r1 - r0) * b,))
+    if mloc:
+        Vs = V.data.view(Tn, Tm, b, b)[:, r0:r1].contiguous()
+        kernel(Vs, mloc, ws)
+    return _gather_vec(ctx, ws, shards)
 
 
 @registry.register("distla.xprod_self")
@@ -286,8 +381,12 @@ def xprod_self(ctx, v_name, out_name):
 @registry.register("distla.xprod_self_diag")
 def xprod_self_diag(ctx, v_name, out_name):
     V = _need(ctx, v_name, "rectangular")
-    d = _alloc(ctx, "vector", V.m)
-    ctx.call("bgp_xprod_self_diag", _ptr(V.data), V.n, V.m, V.tile, _ptr(d), ctx.stream)
+    if ctx.G > 1:
+        d = _sharded_cols(ctx, V, lambda Vs, mloc, ds: ctx.call(
+            "bgp_xprod_self_diag", _ptr(Vs), V.n, mloc, V.tile, _ptr(ds), ctx.stream))
+    else:
+        d = _alloc(ctx, "vector", V.m)
+        ctx.call("bgp_xprod_self_diag", _ptr(V.data), V.n, V.m, V.tile, _ptr(d), ctx.stream)
     ctx.store[out_name] = DevObj("vector", V.col_layout, None, V.tile, d)
 
 

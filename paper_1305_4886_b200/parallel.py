@@ -217,6 +217,33 @@ def dist_trsv(dist, local, y, ops, comm, forward=True):
     return x, comm.min_nonzero(info)
 
 
+def col_shards(T, world):
+    """Contiguous split of T tile rows over `world` ranks: [(r0, r1)] per
+    rank, the first T mod world ranks one row longer.  The kriging RHS
+    columns (tile rows of the transposed rectangular object) are sharded
+    this way: every column is solved independently."""
+    base, extra = divmod(T, world)
+    out, r0 = [], 0
+    for r in range(world):
+        r1 = r0 + base + (1 if r < extra else 0)
+        out.append((r0, r1))
+        r0 = r1
+    return out
+
+
+def gather_col_shards(comm, part, shards, fill):
+    """All-gather per-rank column shards into the full object.
+
+    `part` is this rank's (lead, r1 - r0, ...) slice, padded by the caller
+    to the widest shard along dim 1; `fill(r0, r1, piece)` stores rank r's
+    piece (already cut to its width).  Every rank ends with the full object.
+    """
+    parts = comm.all_gather(part)
+    for (r0, r1), piece in zip(shards, parts):
+        if r1 > r0:
+            fill(r0, r1, piece[:, :r1 - r0])
+
+
 def dist_logdet(dist, local, ops, comm):
     """2 sum log diag(L): per-rank partials summed in rank order."""
     part, info = ops.logdet_partial(local, dist.diag_items())
@@ -247,6 +274,23 @@ class TorchComm:
     def all_reduce_sum(self, tensor):
         if self.world > 1:
             self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def all_gather(self, tensor):
+        """Equal-shaped tensors of every rank, in rank order.  NCCL gathers
+        into one buffer; gloo (the CPU tests, and ranks sharing one GPU)
+        stages device tensors through host memory."""
+        if self.world == 1:
+            return [tensor]
+        import torch
+        t = tensor.contiguous()
+        if t.is_cuda and self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return list(out.unbind(0))
+        host = t.cpu()
+        outs = [torch.empty_like(host) for _ in range(self.world)]
+        self.dist.all_gather(outs, host, group=self.group)
+        return [o.to(t.device) for o in outs]
 
     def all_gather_float(self, value):
         if self.world == 1:

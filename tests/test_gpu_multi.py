@@ -18,6 +18,10 @@ from conftest import relerr, spd_matrix
 
 pytestmark = pytest.mark.gpu
 
+# 23 x 23 = 529 prediction points: 5 tile columns of 128, so the kriging
+# RHS shards are uneven (3 + 2 on two ranks; 2, 1, 1, 1 on four)
+PRED_SIDE = 23
+
 
 def _free_port():
     with socket.socket() as s:
@@ -62,10 +66,11 @@ def _worker(rank, world, port, q):
         # GP log density + kriging (config-1 recipe at n = 900)
         kern, X, theta, extra, z = orc.config_inputs(1, n=900)
         y = np.linalg.cholesky(orc.dense_cov(kern, theta, X, **extra)) @ z
-        Xp = orc.c3_pred_coords(6)
+        Xp = orc.c3_pred_coords(PRED_SIDE)
         prob = KrigeProblem(cl, "g", builtin_spec(kern, X, Xp, **extra), y, theta, m=len(Xp))
         out["ll"] = prob.log_density()
         out["mean"], out["se"] = prob.predict(se_fit=True)
+        out["pv"] = prob.prediction_variance()
         cl.shutdown()
         q.put((rank, out))
     finally:
@@ -104,9 +109,10 @@ def test_multi_rank_path_on_one_gpu(world):
     bvec = np.random.default_rng(5).standard_normal(n)
     kern, X, theta, extra, z = orc.config_inputs(1, n=900)
     y = np.linalg.cholesky(orc.dense_cov(kern, theta, X, **extra)) @ z
-    ref = orc.OracleProblem(kern, X, y, theta, pred_coords=orc.c3_pred_coords(6), **extra)
+    ref = orc.OracleProblem(kern, X, y, theta, pred_coords=orc.c3_pred_coords(PRED_SIDE), **extra)
     want_ll = ref.log_density()
     want_mean, want_se = ref.predict(se_fit=True)
+    want_pv = ref.prediction_variance()
     T = -(-n // 128)
     assert sum(r["owned"] for r in res.values()) == T * (T + 1) // 2
     for r in res.values():
@@ -117,5 +123,6 @@ def test_multi_rank_path_on_one_gpu(world):
         assert abs(r["ll"] - want_ll) <= 1e-10 * abs(want_ll)
         assert relerr(r["mean"], want_mean) <= 1e-9
         assert relerr(r["se"], want_se) <= 1e-9
+        assert relerr(r["pv"], want_pv) <= 1e-9
     lls = [r["ll"] for r in res.values()]
     assert all(v == lls[0] for v in lls)  # identical on every rank

@@ -246,3 +246,85 @@ def test_tile_dist_layout_invariants():
                 assert c == cnt
                 assert [int(I) for I in dists[root].tiles[s:s + c, 0]] == \
                        [I for I in range(J + 1, T) if slot[I] >= off and slot[I] < off + cnt]
+
+
+def test_col_shards_partition():
+    from paper_1305_4886_b200.parallel import col_shards
+    for T in (0, 1, 3, 8, 13, 32):
+        for G in (1, 2, 4, 8):
+            sh = col_shards(T, G)
+            assert len(sh) == G and sh[0][0] == 0 and sh[-1][1] == T
+            assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+            widths = [r1 - r0 for r0, r1 in sh]
+            assert max(widths) - min(widths) <= 1
+
+
+def _rhs_worker(rank, world, port, q):
+    """Kriging solve with RHS columns sharded over ranks (ops.solve_rect at
+    G > 1): each rank solves its tile-row shard of the transposed RHS
+    (Tn, Tm, b, b) storage, then the shards are all-gathered."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_4886_b200.parallel import TorchComm, col_shards, gather_col_shards
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, m, b = 40, 37, 8
+        Tn, Tm = -(-n // b), -(-m // b)
+        L = np.linalg.cholesky(spd_matrix(n, seed=2))
+        B = np.random.default_rng(7).standard_normal((n, m))
+        # transposed storage: tile (I, J) of B^T (m x n) at J*Tm + I, column-major inside
+        Bt = np.zeros((Tm * b, Tn * b))
+        Bt[:m, :n] = B.T
+        tiles = torch.zeros((Tn, Tm, b, b), dtype=torch.float64)
+        for J in range(Tn):
+            for I in range(Tm):
+                tiles[J, I] = torch.from_numpy(Bt[I * b:(I + 1) * b, J * b:(J + 1) * b].T.copy())
+        shards = col_shards(Tm, world)
+        r0, r1 = shards[rank]
+        mine = tiles[:, r0:r1].clone()
+        # local solve of my columns: X^T = B^T L^-T on the dense shard
+        cols = Bt[r0 * b:r1 * b, :n]
+        sol = np.linalg.solve(L, cols.T).T
+        for J in range(Tn):
+            for I in range(r1 - r0):
+                blk = np.zeros((b, b))
+                piece = sol[I * b:(I + 1) * b, J * b:(J + 1) * b]
+                blk[:piece.shape[0], :piece.shape[1]] = piece
+                mine[J, I] = torch.from_numpy(blk.T.copy())
+        width = max(s1 - s0 for s0, s1 in shards)
+        part = torch.zeros((Tn, width, b, b), dtype=torch.float64)
+        part[:, :r1 - r0] = mine
+        full = torch.zeros_like(tiles)
+
+        def fill(s0, s1, piece):
+            full[:, s0:s1] = piece
+        gather_col_shards(TorchComm(), part, shards, fill)
+        Xt = np.zeros((Tm * b, Tn * b))
+        for J in range(Tn):
+            for I in range(Tm):
+                Xt[I * b:(I + 1) * b, J * b:(J + 1) * b] = full[J, I].numpy().T
+        q.put((rank, Xt[:m, :n].T.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_rhs_solve_gathers_full_result(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rhs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    L = np.linalg.cholesky(spd_matrix(40, seed=2))
+    B = np.random.default_rng(7).standard_normal((40, 37))
+    want = np.linalg.solve(L, B)
+    for _, X in out:
+        assert relerr(X, want) <= 1e-12
