@@ -44,9 +44,9 @@ namespace BGP_GEMM_NS {
 
 // Tile configuration.  One CTA per SM, three warpgroups:
 //   WG0  producers: warp 0 feeds consumer group 0's ring, warp 1 group 1's
-//        (setmaxnreg.dec 40);
+//        (setmaxnreg.dec to PRODUCER_REGS);
 //   WG1, WG2  consumers: 4 MMA warps each (2 x 2 warps of 64x32), each group
-//        owns a 128x64 output block at a time (setmaxnreg.inc 232).
+//        owns a 128x64 output block at a time (setmaxnreg.inc to CONSUMER_REGS).
 // The two consumer groups take alternate blocks of the CTA's static schedule
 // and run concurrently, so one group's epilogue overlaps the other group's
 // main loop and the DMMA pipe never drains between blocks.
@@ -55,12 +55,17 @@ constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 16;
 constexpr int GROUPS = 3;
 constexpr int WM = 32, WN = 32;                // warp tile
 constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 144;
+#elif defined(BGP_GEMM_BK16S2)  // probe: 2 stages of BK = 16, whole 64-row warp tile staged at once
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 2, EPI_ROWS = 64;
+constexpr int GROUPS = 2;
+constexpr int WM = 64, WN = 32;
+constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
 #elif defined(BGP_GEMM_BK32)  // 2 stages of BK = 32, epilogue in 16-row rounds
 constexpr int BM = 128, BN = 64, BK = 32, STAGES = 2, EPI_ROWS = 16;
 constexpr int GROUPS = 2;
 constexpr int WM = 64, WN = 32;
 constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
-#else
+#else  // tiles < 512: 3 stages of BK = 16, epilogue in 32-row rounds
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 32;
 constexpr int GROUPS = 2;
 constexpr int WM = 64, WN = 32;
@@ -452,32 +457,22 @@ __device__ __forceinline__ void sts64(uint32_t base, double v) {
 // (row-pair p, column parity e) in box 0, column block j = 0.  NEG stages
 // -acc (integer sign flip, no FP64 instruction); MASK zeroes the strict upper
 // triangle of a diagonal tile (m < n).
-template <int R, bool NEG, bool MASK>
+template <int R, bool NEG, bool MASK, int II = 0, int J = 0>
 __device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const uint32_t (&cb)[2][2], int m0,
                                            int n0) {
   constexpr int NII = EPI_ROWS / 8;
+  if constexpr (II < NII && J < NJ) {
 #pragma unroll
-  for (int ii = 0; ii < NII; ++ii) {
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double v = acc[R * NII + ii][j][e];
-        if (NEG) v = __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull);
-        if (MASK && m0 + ii * 8 < n0 + j * 8 + e) v = 0.0;
-        const uint32_t a = cb[ii & 1][e];
-        switch ((ii >> 1) * NJ + j) {  // immediate offsets: box (ii >> 1), column block j
-          case 0: sts64<0>(a, v); break;
-          case 1: sts64<1024>(a, v); break;
-          case 2: sts64<2048>(a, v); break;
-          case 3: sts64<3072>(a, v); break;
-          case 4: sts64<WBOX_BYTES>(a, v); break;
-          case 5: sts64<WBOX_BYTES + 1024>(a, v); break;
-          case 6: sts64<WBOX_BYTES + 2048>(a, v); break;
-          default: sts64<WBOX_BYTES + 3072>(a, v); break;
-        }
-      }
+    for (int e = 0; e < 2; ++e) {
+      double v = acc[R * NII + II][J][e];
+      if (NEG) v = __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull);
+      if (MASK && m0 + II * 8 < n0 + J * 8 + e) v = 0.0;
+      // immediate offset: box (II >> 1), column block J
+      sts64<(II >> 1) * WBOX_BYTES + J * 1024>(cb[II & 1][e], v);
     }
+    stage_rows<R, NEG, MASK, II, J + 1>(acc, cb, m0, n0);
+  } else if constexpr (II < NII) {
+    stage_rows<R, NEG, MASK, II + 1, 0>(acc, cb, m0, n0);
   }
 }
 
@@ -485,7 +480,8 @@ __device__ __forceinline__ void stage_rows(const double (&acc)[MI][NJ][2], const
 template <int R>
 __device__ __forceinline__ void stage_round(const double (&acc)[MI][NJ][2], const uint32_t (&cb)[2][2], int m0,
                                             int n0, bool store, bool lower) {
-  if (store) {
+  if constexpr (R >= EPI_ROUNDS) return;
+  else if (store) {
     if (lower) stage_rows<R, false, true>(acc, cb, m0, n0);
     else stage_rows<R, false, false>(acc, cb, m0, n0);
   } else {

@@ -76,7 +76,7 @@ def main():
         if hasattr(lib, "bgp_probe_trace"):
             buf = np.zeros((148, 2, 64, 3), dtype=np.uint64)
             lib.bgp_probe_trace(ctypes.c_void_p(buf.ctypes.data))
-            np.save(os.path.join(ROOT, "gpurun_out", "probe", "trace.npy"), buf)
+            np.save(os.path.join(ROOT, "gpurun_out", "probe", "trace_" + os.path.basename(path)[:-3] + ".npy"), buf)
         lib.bgp_finalize(ctx)
 
 
