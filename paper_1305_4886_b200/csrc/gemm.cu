@@ -86,10 +86,20 @@ constexpr int EPI_ROUNDS = WM / EPI_ROWS;      // rounds per warp tile
 constexpr int WSTAGE_BYTES = EPI_BOXES * WBOX_BYTES;  // a warp's epilogue slice (one round)
 constexpr int HALVES = BK / 4;                 // k4 half-steps per stage
 constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;
+// When a warp's other epilogue rounds fit in its quarter of one operand stage,
+// the epilogue stages them in the block's last stage (released to the
+// producer only once the bulk reads are done, early in the next block) and
+// the last round in the warp's own slice: no wait between rounds.
+#if defined(BGP_EXP_NO_EPI) || defined(BGP_EPI_RED) || defined(BGP_EXP_EPI_SLICE)
+constexpr bool EPI_IN_STAGE = false;
+#else
+constexpr bool EPI_IN_STAGE = STAGE_BYTES >= GROUP_WARPS * (EPI_ROUNDS - 1) * WSTAGE_BYTES && EPI_ROUNDS > 1;
+#endif
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
-constexpr int BAR_BYTES = 256;
+constexpr int BAR_BYTES = 512;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 32 <= BAR_BYTES, "barrier area");
 
 #ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
 constexpr int TRACE_ITEMS = 64;
@@ -309,12 +319,22 @@ __device__ __forceinline__ uint32_t lane_off(int p, int t, int q, int s4) {
   return (uint32_t)(k * 128 + ((((p << 2) ^ ((q >> 1) ^ k)) & 7) << 4) + ((q & 1) << 3));
 }
 
+// What the consumers need of a block, decoded once by the producer and
+// handed over with the block's first stage (written before the `full` arrive)
+struct BlockSlot {
+  int valid;  // 0: no more work
+  int cTile, mrow0, nrow0;
+  int nk;     // BK stages
+  int lower, store, gate;
+};
+static_assert(sizeof(BlockSlot) == 32, "slot size");
+
 struct GroupSmem {
   uint8_t* stages;
   uint8_t* cbuf;
   uint64_t* full;
   uint64_t* empty;
-  int64_t* slot;  // per stage: block id (task * 64 + pass) starting there, -1: no more work
+  BlockSlot* slot;  // per stage: the block starting there
 };
 
 __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
@@ -324,7 +344,7 @@ __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES);
   gs.full = bars;
   gs.empty = bars + STAGES;
-  gs.slot = reinterpret_cast<int64_t*>(bars + GROUPS * 2 * STAGES + 1 - g * (2 * STAGES)) + g * STAGES;
+  gs.slot = reinterpret_cast<BlockSlot*>(smem + GROUPS * GROUP_BYTES + 256) + g * STAGES;
   return gs;
 }
 
@@ -373,7 +393,17 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&gs.empty[stage], phase ^ 1);
-        if (kc == 0) gs.slot[stage] = task * 64 + pass;  // read by the consumers after `full`
+        if (kc == 0) {  // read by the consumers after `full`
+          BlockSlot& sl = gs.slot[stage];
+          sl.valid = 1;
+          sl.cTile = it.cTile;
+          sl.mrow0 = it.mrow0;
+          sl.nrow0 = it.nrow0;
+          sl.nk = nk;
+          sl.lower = it.lower;
+          sl.store = it.store;
+          sl.gate = it.gate;
+        }
 #ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
         mbar_arrive(&gs.full[stage]);
 #else
@@ -401,7 +431,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
   }
   // no more work: hand the consumers a sentinel through the next stage
   mbar_wait(&gs.empty[stage], phase ^ 1);
-  gs.slot[stage] = -1;
+  gs.slot[stage].valid = 0;
   mbar_arrive(&gs.full[stage]);
 }
 
@@ -492,15 +522,16 @@ __device__ __forceinline__ void stage_round(const double (&acc)[MI][NJ][2], cons
 
 // half-steps H .. HALVES-2 of a stage: load the fragments of H+1, issue the
 // DMMAs of H (compile-time recursion so every offset is an immediate)
-template <int H>
+template <int H, typename Hook>
 __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ][2], const uint32_t (&offA)[2][2],
-                                             const uint32_t (&offB)[2][2], uint32_t sb) {
+                                             const uint32_t (&offB)[2][2], uint32_t sb, Hook&& hook) {
   if constexpr (H + 1 < HALVES) {
     constexpr int N = H + 1;
     load_frag<(N >> 1)>(f[N & 1], offA[0][N & 1] + sb, offA[1][N & 1] + sb, offB[0][N & 1] + sb,
                         offB[1][N & 1] + sb);
     mma_frag(acc, f[H & 1]);
-    stage_halves<H + 1>(f, acc, offA, offB, sb);
+    if constexpr (H == 2) hook();  // a few k4 steps into the stage
+    stage_halves<H + 1>(f, acc, offA, offB, sb, hook);
   }
 }
 
@@ -510,7 +541,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   static_assert((MI == 8 || MI == 4) && NJ == 4 && WN / 16 == 2, "load_frag: 64x32 or 32x32 warp tiles");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
-  const int kc_per_tile = p.b / BK;
   // per-lane shared addresses of the fragments in stage 0 (t = k4 half-step)
   const uint32_t st0 = smem_u32(gs.stages);
   uint32_t offA[2][2], offB[2][2];
@@ -522,14 +552,26 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       offB[pp][t] = st0 + (uint32_t)(STAGE_A_BYTES + wn * (WN / 16) * BOX_BYTES) + lane_off(pp, t, q, s4);
     }
   uint8_t* cw = gs.cbuf + gwarp * WSTAGE_BYTES;
-  uint32_t cbase[2][2];
+  uint32_t coff[2][2];
 #pragma unroll
   for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) cbase[pp][e] = smem_u32(cw) + lane_off(pp, e, q, s4);
+    for (int e = 0; e < 2; ++e) coff[pp][e] = lane_off(pp, e, q, s4);
   int stage = 0;
   uint32_t phase = 0;
   bool store_pending = false;
+  int held = -1;  // EPI_IN_STAGE: stage still holding this warp's epilogue rows
+  // release the held stage once its bulk reads are done (early in the next block)
+  auto release_held = [&]() {
+    if (EPI_IN_STAGE && held >= 0) {
+      if (lane == 0) {
+        tma_store_wait_read0();
+        mbar_arrive(&gs.empty[held]);
+      }
+      __syncwarp();
+      held = -1;
+    }
+  };
   const uint64_t pol_stream = l2_policy_evict_first();
   // Stagger: every block costs the same, so two groups that start together
   // would hit their epilogues together and leave the DMMA pipe idle.  Group 1
@@ -547,10 +589,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 
   for (;;) {
     mbar_wait(&gs.full[stage], phase);  // first stage of the next block (or the sentinel)
-    const int64_t slot = gs.slot[stage];
-    if (slot < 0) break;
-    const Item it = gemm_decode(p, slot >> 6, (int)(slot & 63));
-    const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
+    const BlockSlot it = gs.slot[stage];
+    if (!it.valid) break;
+    const int nk = it.nk;
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -576,7 +617,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         if (lane == 0) mbar_arrive(stagger);
         stagger_arrive = false;
       }
-      stage_halves<0>(f, acc, offA, offB, sb);
+      stage_halves<0>(f, acc, offA, offB, sb, release_held);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
@@ -590,10 +631,17 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[cur]);
     }
-    stage_halves<0>(f, acc, offA, offB, sb);
+    stage_halves<0>(f, acc, offA, offB, sb, release_held);
     mma_frag(acc, f[(HALVES - 1) & 1]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&gs.empty[stage]);
+    const int last = stage;
+    if constexpr (EPI_IN_STAGE) {
+      // every warp of the group has read its fragments out of the last
+      // stage before any warp overwrites it with epilogue rows
+      named_bar_sync(3 + g, 32 * GROUP_WARPS);
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gs.empty[stage]);
+    }
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
@@ -650,31 +698,55 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 #else
 #pragma unroll
     for (int r = 0; r < EPI_ROUNDS; ++r) {
-      if (lane == 0 && (store_pending || r > 0)) tma_store_wait_read0();  // slice free again
+      // rounds 0 .. EPI_ROUNDS-2 go to the warp's quarter of the last stage
+      // (EPI_IN_STAGE), the last round to its own slice; otherwise every
+      // round reuses the slice once the previous round's boxes were read
+      auto round_buf = [&](int rr) -> uint8_t* {
+        return (EPI_IN_STAGE && rr + 1 < EPI_ROUNDS)
+                   ? gs.stages + last * STAGE_BYTES + (gwarp * (EPI_ROUNDS - 1) + rr) * WSTAGE_BYTES
+                   : cw;
+      };
+      uint8_t* wbuf = round_buf(r);
+      // (EPI_IN_STAGE: the previous block's reads were waited for when its
+      // stage was released, so nothing is pending here)
+      if (!EPI_IN_STAGE && lane == 0 && (store_pending || r > 0)) tma_store_wait_read0();  // slice free
       __syncwarp();
+      uint32_t cb[2][2];
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) cb[pp][e] = smem_u32(wbuf) + coff[pp][e];
       // row m = m0 + ii*8 of the round, column n = n0 + j*8 + e (tile coordinates)
       const int m0 = it.mrow0 + wm * WM + r * EPI_ROWS + q, n0 = it.nrow0 + wn * WN + 2 * s4;
       switch (r) {
-        case 0: stage_round<0>(acc, cbase, m0, n0, it.store, it.lower); break;
-        case 1: stage_round<1>(acc, cbase, m0, n0, it.store, it.lower); break;
-        case 2: stage_round<2>(acc, cbase, m0, n0, it.store, it.lower); break;
-        default: stage_round<3>(acc, cbase, m0, n0, it.store, it.lower); break;
+        case 0: stage_round<0>(acc, cb, m0, n0, it.store, it.lower); break;
+        case 1: stage_round<1>(acc, cb, m0, n0, it.store, it.lower); break;
+        case 2: stage_round<2>(acc, cb, m0, n0, it.store, it.lower); break;
+        default: stage_round<3>(acc, cb, m0, n0, it.store, it.lower); break;
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        const int r0 = it.mrow0 + wm * WM + r * EPI_ROWS, c0 = it.nrow0 + wn * WN;
+      // EPI_IN_STAGE: every round is staged first, then one proxy fence and
+      // all boxes; otherwise each round is fenced and sent on its own
+      if (!EPI_IN_STAGE || r + 1 == EPI_ROUNDS) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int rr = EPI_IN_STAGE ? 0 : r; rr <= r; ++rr) {
+            uint8_t* rb = round_buf(rr);
+            const int r0 = it.mrow0 + wm * WM + rr * EPI_ROWS, c0 = it.nrow0 + wn * WN;
 #pragma unroll
-        for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
-          if (it.store)
-            tma_store_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
-          else
-            tma_reduce_add_3d(tmC, cw + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+            for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
+              if (it.store)
+                tma_store_3d(tmC, rb + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+              else
+                tma_reduce_add_3d(tmC, rb + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+            }
+          }
+          tma_store_commit();
         }
-        tma_store_commit();
       }
     }
     store_pending = true;
+    if constexpr (EPI_IN_STAGE) held = last;
 #endif
 #ifndef BGP_EPI_RED
     // Column-(J+1) gates: a warp signals a block once its bulk reduction has
@@ -697,6 +769,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 #endif
   }
   if (stagger_arrive && lane == 0) mbar_arrive(stagger);
+  release_held();
   if (lane == 0 && store_pending) tma_store_wait_all0();
 }
 

@@ -11,6 +11,8 @@ if [ "$1" = "build" ]; then
       NO_TMA_NO_EPI) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       TRACE) F="-DBGP_EXP_TRACE";;
       BK32) F="-DBGP_GEMM_BK32";;
+      BK32_SLICE) F="-DBGP_GEMM_BK32 -DBGP_EXP_EPI_SLICE";;
+      BK32_SLICE_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_EPI_SLICE -DBGP_EXP_TRACE";;
       BK16S2) F="-DBGP_GEMM_BK16S2";;
       BK16S2_TRACE) F="-DBGP_GEMM_BK16S2 -DBGP_EXP_TRACE";;
       BK32_RED) F="-DBGP_GEMM_BK32 -DBGP_EPI_RED";;
