@@ -103,7 +103,7 @@ static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 32
 
 #ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
 constexpr int TRACE_ITEMS = 64;
-__device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][3];
+__device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][6];
 #endif
 
 struct Item {
@@ -638,6 +638,10 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       // every warp of the group has read its fragments out of the last
       // stage before any warp overwrites it with epilogue rows
       named_bar_sync(3 + g, 32 * GROUP_WARPS);
+#ifdef BGP_EXP_TRACE
+      if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+        g_trace[blockIdx.x][g][t_idx][3] = clock64();
+#endif
     } else {
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[stage]);
@@ -701,12 +705,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       // rounds 0 .. EPI_ROUNDS-2 go to the warp's quarter of the last stage
       // (EPI_IN_STAGE), the last round to its own slice; otherwise every
       // round reuses the slice once the previous round's boxes were read
-      auto round_buf = [&](int rr) -> uint8_t* {
-        return (EPI_IN_STAGE && rr + 1 < EPI_ROUNDS)
-                   ? gs.stages + last * STAGE_BYTES + (gwarp * (EPI_ROUNDS - 1) + rr) * WSTAGE_BYTES
-                   : cw;
-      };
-      uint8_t* wbuf = round_buf(r);
+      const bool in_stage = EPI_IN_STAGE && r + 1 < EPI_ROUNDS;
+      uint8_t* wbuf = in_stage ? gs.stages + last * STAGE_BYTES + (gwarp * (EPI_ROUNDS - 1) + r) * WSTAGE_BYTES
+                               : cw;
       // (EPI_IN_STAGE: the previous block's reads were waited for when its
       // stage was released, so nothing is pending here)
       if (!EPI_IN_STAGE && lane == 0 && (store_pending || r > 0)) tma_store_wait_read0();  // slice free
@@ -724,25 +725,26 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         case 2: stage_round<2>(acc, cb, m0, n0, it.store, it.lower); break;
         default: stage_round<3>(acc, cb, m0, n0, it.store, it.lower); break;
       }
-      // EPI_IN_STAGE: every round is staged first, then one proxy fence and
-      // all boxes; otherwise each round is fenced and sent on its own
-      if (!EPI_IN_STAGE || r + 1 == EPI_ROUNDS) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          for (int rr = EPI_IN_STAGE ? 0 : r; rr <= r; ++rr) {
-            uint8_t* rb = round_buf(rr);
-            const int r0 = it.mrow0 + wm * WM + rr * EPI_ROWS, c0 = it.nrow0 + wn * WN;
+#ifdef BGP_EXP_TRACE
+      if (r == 0 && gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+        g_trace[blockIdx.x][g][t_idx][4] = clock64();
+#endif
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int r0 = it.mrow0 + wm * WM + r * EPI_ROWS, c0 = it.nrow0 + wn * WN;
 #pragma unroll
-            for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
-              if (it.store)
-                tma_store_3d(tmC, rb + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
-              else
-                tma_reduce_add_3d(tmC, rb + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
-            }
-          }
-          tma_store_commit();
+        for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
+          if (it.store)
+            tma_store_3d(tmC, wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
+          else
+            tma_reduce_add_3d(tmC, wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
         }
+        tma_store_commit();
+#ifdef BGP_EXP_TRACE
+        if (r == 0 && gwarp == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
+          g_trace[blockIdx.x][g][t_idx][5] = clock64();
+#endif
       }
     }
     store_pending = true;

@@ -74,7 +74,7 @@ def main():
                                   "us": round(us, 1), "tflops": round(fl / us / 1e6, 2)}), flush=True)
                 del V, S
         if hasattr(lib, "bgp_probe_trace"):
-            buf = np.zeros((148, 2, 64, 3), dtype=np.uint64)
+            buf = np.zeros((148, 2, 64, 6), dtype=np.uint64)
             lib.bgp_probe_trace(ctypes.c_void_p(buf.ctypes.data))
             np.save(os.path.join(ROOT, "gpurun_out", "probe", "trace_" + os.path.basename(path)[:-3] + ".npy"), buf)
         lib.bgp_finalize(ctx)
