@@ -125,13 +125,13 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def dist_setup(impl):
+def dist_setup(impl, share_gpu=False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        if impl == "reference":
+        if impl == "reference" or share_gpu:
             dist.init_process_group("gloo")
         else:
             local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -221,7 +221,7 @@ def run_b200(args, world, rank):
 
     X, y, sc = load_c4()
     n = len(y)
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.debug_share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     cl = spawn(world, tile=args.tile, device=local)
     dev = cl.device
     spec = builtin_spec("matern-nugget", X, nu=0.5)
@@ -272,12 +272,35 @@ def run_b200(args, world, rank):
     if prof[7] == 0:  # sharded path: host-synchronised time of the last factorization
         chol_ms = max_over_ranks(cl.last_cholesky_ms or 0.0, world)
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    peak = FP64_DMMA_PEAK
+    roof_kernel = "gemm_dmma_kernel (trailing SYRK/GEMM)"
+    if world > 1:  # aggregate: the whole factorization against N x the per-GPU peak
+        gemm_tflops = n ** 3 / 3 / (chol_ms / 1e3) / 1e12 if chol_ms else 0.0
+        gemm_flops, facts = n ** 3 / 3, 1
+        peak = FP64_DMMA_PEAK * world
+        roof_kernel = f"distributed Cholesky, aggregate over {world} GPUs (n^3/3 per factorization)"
     phases = {"cholesky_ms_per_eval": chol_ms, "potrf_ms_per_eval": potrf_ms / facts,
               "potrf_exposed_ms_per_eval": prof[9] / facts,
               "trsm_ms_per_eval": trsm_ms / facts, "gemm_ms_per_eval": gemm_ms / facts,
               "eval_ms": ms / args.steps,
               "other_ms_per_eval": ms / args.steps - chol_ms,
               "gemm_share_of_step": (gemm_ms / facts) / (ms / args.steps)}
+
+    # G > 1: one more (untimed) evaluation with CUDA-event spans around the
+    # panel broadcasts and the trailing updates -> exposed communication
+    comm = None
+    if world > 1:
+        cl.comm_timeline = True
+        step += 1
+        prob.log_density(theta_k(step))
+        cl.comm_timeline = False
+        c = cl.last_comm or {}
+        comm = {"comm_ms": max_over_ranks(c.get("comm_ms", 0.0), world),
+                "exposed_comm_ms": max_over_ranks(c.get("exposed_comm_ms", 0.0), world),
+                "collectives_per_rank": c.get("collectives", 0),
+                "how": "CUDA events around each NCCL broadcast (side stream) and each trailing "
+                       "update (compute stream) of one untimed evaluation; exposed = broadcast "
+                       "time not covered by any update; max over ranks"}
 
     # end to end through the public API from host buffers (pinned), every step
     # uploads coords + y and reads back the scalars
@@ -327,9 +350,9 @@ def run_b200(args, world, rank):
                              "covariance (>> 126 MB L2)"},
             "cholesky_tflops": n ** 3 / 3 / (chol_ms / 1e3) / 1e12 if chol_ms else None,
             "phases": phases,
-            "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (trailing SYRK/GEMM)",
-                         "achieved": gemm_tflops, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
-                         "frac": gemm_tflops / FP64_DMMA_PEAK, "traffic": traffic, "traffic_source": traffic_src,
+            "roofline": {"bound": "tensor", "kernel": roof_kernel,
+                         "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": gemm_tflops / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": "measured DMMA.8x8x4 loop (profiles/r01_fp64_peaks.jsonl); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "algorithmic_flops_per_eval": gemm_flops / facts,
@@ -341,6 +364,8 @@ def run_b200(args, world, rank):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if comm is not None:
+            line["communication"] = comm
         print(json.dumps(line), flush=True)
     cl.shutdown()
 
@@ -355,8 +380,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-samples", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--debug-share-gpu", action="store_true",
+                    help="test only: every rank on cuda:0 over gloo, to exercise the N > 1 path "
+                         "on a one-GPU box (the numbers mean nothing)")
     args = ap.parse_args()
-    world, rank = dist_setup(args.impl)
+    world, rank = dist_setup(args.impl, args.debug_share_gpu)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -263,12 +263,19 @@ def cholesky(ctx, name, out_name):
     try:
         if obj.dist is not None:
             import time
-            from ..parallel import dist_cholesky
+            from ..parallel import LibTileOps, Timeline, dist_cholesky
+            # ctx.comm_timeline: record comm / compute spans (exposed-comm report)
+            tl = Timeline(ctx.device) if getattr(ctx, "comm_timeline", False) else None
+            ctx.comm.timeline = tl
             ctx.synchronize()
             t0 = time.perf_counter()
-            info.value = dist_cholesky(obj.dist, obj.data, _tile_ops(ctx, obj.n), ctx.comm)
+            try:
+                info.value = dist_cholesky(obj.dist, obj.data, LibTileOps(ctx, obj.n, tl), ctx.comm)
+            finally:
+                ctx.comm.timeline = None
             ctx.synchronize()
             ctx.last_cholesky_ms = 1e3 * (time.perf_counter() - t0)
+            ctx.last_comm = tl.summary() if tl is not None else None
         else:
             ctx.call("bgp_potrf", _ptr(obj.data), obj.n, obj.tile, ctypes.byref(info), ctx.stream)
     except BaseException:

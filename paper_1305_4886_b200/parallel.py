@@ -251,6 +251,62 @@ def dist_logdet(dist, local, ops, comm):
     return float(sum(parts)), comm.min_nonzero(info)
 
 
+def exposed_time(comm, compute):
+    """Total length of the `comm` intervals not covered by the union of the
+    `compute` intervals (lists of (start, end)): the communication time the
+    schedule failed to hide (SURVEY.md 8d, C5 "exposed NVLink time")."""
+    cover = []
+    for a, b in sorted(compute):
+        if cover and a <= cover[-1][1]:
+            cover[-1][1] = max(cover[-1][1], b)
+        else:
+            cover.append([a, b])
+    total = 0.0
+    for a, b in comm:
+        hidden = sum(max(0.0, min(b, y) - max(a, x)) for x, y in cover)
+        total += (b - a) - hidden
+    return total
+
+
+class Timeline:
+    """CUDA-event spans of a distributed factorization: "comm" around each
+    collective (recorded on the stream that issues it) and "compute" around
+    each trailing update.  summary() syncs and reports milliseconds."""
+
+    def __init__(self, device):
+        self.device = device
+        self.spans = []
+        self._origin = None
+
+    def span(self, kind):
+        import contextlib
+
+        import torch
+
+        @contextlib.contextmanager
+        def rec():
+            if self._origin is None:
+                self._origin = torch.cuda.Event(enable_timing=True)
+                self._origin.record(torch.cuda.current_stream(self.device))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(self.device))
+            yield
+            e1.record(torch.cuda.current_stream(self.device))
+            self.spans.append((kind, e0, e1))
+        return rec()
+
+    def summary(self):
+        import torch
+        torch.cuda.synchronize(self.device)
+        iv = {"comm": [], "compute": []}
+        for kind, e0, e1 in self.spans:
+            iv[kind].append((self._origin.elapsed_time(e0), self._origin.elapsed_time(e1)))
+        comm = sum(b - a for a, b in iv["comm"])
+        return {"comm_ms": comm, "collectives": len(iv["comm"]),
+                "exposed_comm_ms": exposed_time(iv["comm"], iv["compute"])}
+
+
 class TorchComm:
     """Collectives over a torch.distributed process group (NCCL on GPUs,
     gloo in the CPU tests)."""
@@ -260,10 +316,15 @@ class TorchComm:
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
+        self.timeline = None  # Timeline: spans around the panel broadcasts
 
     def broadcast(self, tensor, src):
         if self.world > 1:
-            self.dist.broadcast(tensor, src, group=self.group)
+            if self.timeline is not None:
+                with self.timeline.span("comm"):
+                    self.dist.broadcast(tensor, src, group=self.group)
+            else:
+                self.dist.broadcast(tensor, src, group=self.group)
 
     def reduce_sum(self, tensor, dst):
         # all-reduce (not reduce): 2 KB per step, and it is supported by every
@@ -311,10 +372,11 @@ class TorchComm:
 class LibTileOps:
     """Tile operations of the distributed schedule on this rank's GPU (libbgp)."""
 
-    def __init__(self, cluster, n):
+    def __init__(self, cluster, n, timeline=None):
         self.cl = cluster
         self.b = cluster.tile
         self.n = n
+        self.timeline = timeline  # Timeline: spans around the trailing updates
 
     # buffers ---------------------------------------------------------------
     def empty(self, shape):
@@ -407,6 +469,13 @@ class LibTileOps:
             dev, count = self._items(items), len(items)
         if count == 0:
             return
+        if self.timeline is not None:
+            with self.timeline.span("compute"):
+                self._update(local, panel, dev, count, reserve)
+        else:
+            self._update(local, panel, dev, count, reserve)
+
+    def _update(self, local, panel, dev, count, reserve):
         if reserve:
             self.cl.call("bgp_tile_update_limited", self._p(local), self._p(panel), self._p(panel),
                          self._p(dev), count, self.b, self.cl.num_sms - self.RESERVE_SMS, self.cl.stream)

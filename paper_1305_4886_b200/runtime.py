@@ -77,6 +77,8 @@ class B200Cluster:
                                        "G": G, "tile": self.tile, "seed": seed}}
         self._dev_inputs = {}
         self.last_cholesky_ms = None
+        self.comm_timeline = False  # G > 1: record comm / compute spans of the factorization
+        self.last_comm = None       # their summary (parallel.Timeline.summary)
         self.stream_pos = 0  # draws consumed from this rank's normal stream
         self.events = []
         self.events_enabled = False

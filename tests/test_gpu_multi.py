@@ -46,7 +46,10 @@ def _worker(rank, world, port, q):
         A = spd_matrix(n, seed=5)
         lay = distla.make_layout(n, cl.grid, h=2)
         C = distla.distribute(cl, "C", A, "triangular", lay)
+        cl.comm_timeline = True  # CUDA-event spans of broadcasts and updates
         L, stats = distla.distributed_cholesky(cl, C, "L")
+        cl.comm_timeline = False
+        out["comm"] = cl.last_comm
         out["L"] = distla.collect(cl, L)
         bvec = np.random.default_rng(5).standard_normal(n)
         bd = distla.distribute(cl, "b", bvec, "vector", lay)
@@ -120,6 +123,8 @@ def test_multi_rank_path_on_one_gpu(world):
         assert relerr(r["x"], np.linalg.solve(A, bvec)) <= 1e-10
         assert abs(r["logdet"] - np.linalg.slogdet(A)[1]) <= 1e-12 * abs(r["logdet"])
         assert r["npd"] == 1 and "Ln" not in r["ls"] and "Cn" not in r["ls"]
+        c = r["comm"]
+        assert c["collectives"] > 0 and 0.0 <= c["exposed_comm_ms"] <= c["comm_ms"] + 1e-6
         assert abs(r["ll"] - want_ll) <= 1e-10 * abs(want_ll)
         assert relerr(r["mean"], want_mean) <= 1e-9
         assert relerr(r["se"], want_se) <= 1e-9

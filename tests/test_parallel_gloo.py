@@ -328,3 +328,13 @@ def test_sharded_rhs_solve_gathers_full_result(world):
     want = np.linalg.solve(L, B)
     for _, X in out:
         assert relerr(X, want) <= 1e-12
+
+
+def test_exposed_time_intervals():
+    from paper_1305_4886_b200.parallel import exposed_time
+    assert exposed_time([], [(0, 5)]) == 0
+    assert exposed_time([(0, 2)], []) == 2
+    assert exposed_time([(1, 2)], [(0, 5)]) == 0                 # fully hidden
+    assert exposed_time([(4, 7)], [(0, 5)]) == 2                 # tail exposed
+    assert exposed_time([(0, 10)], [(1, 2), (2, 4), (6, 7)]) == 6  # merged cover
+    assert exposed_time([(0, 3), (5, 9)], [(2, 6), (8, 20)]) == 2 + 2
