@@ -915,11 +915,12 @@ int groups();
 }  // namespace bk32
 
 static bool use_bk32(int b) {
-  static const bool force16 = [] {
+  static const int force = [] {  // BGP_GEMM_CFG=16 / 32 (diagnostics): one configuration everywhere
     const char* e = getenv("BGP_GEMM_CFG");
-    return e && atoi(e) == 16;
+    return e ? atoi(e) : 0;
   }();
-  return b >= 512 && !force16;
+  (void)b;
+  return force != 16;
 }
 
 void gemm_block_counts(int b, int* tile_need, int* diag_need, int* groups_per_cta) {
@@ -939,9 +940,10 @@ void gemm_prepare() {
   bk32::prepare();
 }
 
-// 512 tiles: BK = 32 stages (half the barrier and TMA operations per DMMA);
-// smaller tiles keep BK = 16 (measured: C4 at b = 512 +0.9 %, b = 256 -1.7 %).
-// BGP_GEMM_CFG=16 (diagnostics) forces the first configuration everywhere.
+// Every tile size runs the BK = 32 configuration (half the barrier and TMA
+// operations per DMMA, epilogue staged in the last stage).  Measured on C4:
+// b = 512 +0.9 % over BK = 16 (before the in-stage epilogue), b = 256 +3.0 %
+// (with it; -1.7 % before).  BGP_GEMM_CFG=16 (diagnostics) forces BK = 16.
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
   if (use_bk32(p.b)) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
