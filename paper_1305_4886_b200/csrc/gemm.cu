@@ -101,6 +101,10 @@ constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 32 <= BAR_BYTES, "barrier area");
 
+#ifdef BGP_EXP_STRACE  // probe build: per-stage timestamps (implies the per-item trace)
+#define BGP_EXP_TRACE
+__device__ unsigned long long g_strace[148][2][64][20];
+#endif
 #ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
 constexpr int TRACE_ITEMS = 64;
 __device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][6];
@@ -623,6 +627,10 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         phase ^= 1;
       }
       sb = (uint32_t)stage * STAGE_BYTES;
+#ifdef BGP_EXP_STRACE
+      if (gwarp == 0 && lane == 0 && t_idx < 64 && kc < 19 && blockIdx.x < 148 && g < 2)
+        g_strace[blockIdx.x][g][t_idx][kc] = clock64();
+#endif
 #ifndef BGP_EXP_NO_STAGE_WAIT  // probe build (with NO_TMA): no per-stage wait
       mbar_wait(&gs.full[stage], phase);
 #endif
@@ -955,5 +963,10 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
 #if defined(BGP_EXP_TRACE) && !defined(BGP_GEMM_SECONDARY)
 extern "C" int bgp_probe_trace(void* host_out) {
   return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_trace, sizeof(bgp::bk16::g_trace));
+}
+#endif
+#if defined(BGP_EXP_STRACE) && !defined(BGP_GEMM_SECONDARY)
+extern "C" int bgp_probe_strace(void* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_strace, sizeof(bgp::bk16::g_strace));
 }
 #endif

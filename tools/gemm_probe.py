@@ -77,6 +77,10 @@ def main():
             buf = np.zeros((148, 2, 64, 6), dtype=np.uint64)
             lib.bgp_probe_trace(ctypes.c_void_p(buf.ctypes.data))
             np.save(os.path.join(ROOT, "gpurun_out", "probe", "trace_" + os.path.basename(path)[:-3] + ".npy"), buf)
+        if hasattr(lib, "bgp_probe_strace"):
+            buf = np.zeros((148, 2, 64, 20), dtype=np.uint64)
+            lib.bgp_probe_strace(ctypes.c_void_p(buf.ctypes.data))
+            np.save(os.path.join(ROOT, "gpurun_out", "probe", "strace_" + os.path.basename(path)[:-3] + ".npy"), buf)
         lib.bgp_finalize(ctx)
 
 

@@ -27,6 +27,7 @@ if [ "$1" = "build" ]; then
       G3) F="-DBGP_GEMM_3G";;
       G3_CORE) F="-DBGP_GEMM_3G -DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI";;
       BK32_TRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_TRACE";;
+      BK32_STRACE) F="-DBGP_GEMM_BK32 -DBGP_EXP_STRACE";;
       BK32_NOSTAG) F="-DBGP_GEMM_BK32 -DBGP_EXP_NO_STAGGER";;
       BK32_EVN) F="-DBGP_GEMM_BK32 -DBGP_EXP_EVICT_NORMAL";;
       NO_BAR_TRACE) F="-DBGP_EXP_NO_TMA -DBGP_EXP_NO_EPI -DBGP_EXP_NO_BAR -DBGP_EXP_TRACE";;
