@@ -303,9 +303,13 @@ def run_b200(args, world, rank):
         comm = {"comm_ms": max_over_ranks(c.get("comm_ms", 0.0), world),
                 "exposed_comm_ms": max_over_ranks(c.get("exposed_comm_ms", 0.0), world),
                 "collectives_per_rank": c.get("collectives", 0),
-                "how": "CUDA events around each NCCL broadcast (side stream) and each trailing "
-                       "update (compute stream) of one untimed evaluation; exposed = broadcast "
-                       "time not covered by any update; max over ranks"}
+                "panel_exchange": ("fused TRSM + NVLink peer stores (bgp_panel_trsm_push)"
+                                   if cl.__dict__.get("_panel_xchg", {}).get("x") is not None
+                                   and cl._panel_xchg["x"].ok else "NCCL broadcasts"),
+                "how": "CUDA events around each collective (inverse broadcast, panel broadcasts or "
+                       "push barriers; side stream) and each trailing update (compute stream) of one "
+                       "untimed evaluation; exposed = collective time not covered by any update; "
+                       "max over ranks"}
 
     # end to end through the public API from host buffers (pinned), every step
     # uploads coords + y and reads back the scalars

@@ -243,6 +243,25 @@ int bgp_tile_logdet(bgp_ctx_t ctx, const double* base, const int32_t* diag,
                     int64_t* info, void* stream);
 int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count,
                    int tile, void* stream);
+
+/* Multi-GPU panel push (replaces the NCCL panel broadcast of the sweep,
+ * kernels.py:165-187 send / 175-180 receive): panel buffers are allocated
+ * here, exported as CUDA IPC handles (BGP_IPC_HANDLE_BYTES), and opened by
+ * every peer process (NVLink P2P mappings).  bgp_panel_trsm_push is
+ * bgp_panel_trsm_inv whose epilogue also stores every solved block into tile
+ * slot0 + t of each of the ndst (<= 8) destination buffers dst[] (own and
+ * peer panel buffers, each dst_tiles tiles) from the same staged rows: the
+ * solve and the exchange are one kernel.  The caller orders the receivers'
+ * reads after the kernel (a stream-ordered barrier) and the writes after the
+ * receivers' last use of the buffer. */
+#define BGP_IPC_HANDLE_BYTES 64
+int bgp_ipc_alloc(bgp_ctx_t ctx, size_t bytes, void** ptr, void* handle);
+int bgp_ipc_open(bgp_ctx_t ctx, const void* handle, void** ptr);
+int bgp_ipc_close(bgp_ctx_t ctx, void* ptr);
+int bgp_ipc_free(bgp_ctx_t ctx, void* ptr);
+int bgp_panel_trsm_push(bgp_ctx_t ctx, const double* linv, double* A, int64_t count,
+                        int tile, double* const* dst, int ndst, int64_t slot0,
+                        int64_t dst_tiles, void* stream);
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
                     const double* Bbase, const int32_t* triples /*device, 4 per*/,
                     int64_t count, int tile, void* stream);

@@ -71,6 +71,12 @@ SIGNATURES = {
     "bgp_info_read": (_int, [ctypes.c_void_p, ctypes.POINTER(_i64), _c_dp]),
     "bgp_tile_potrf_async": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, _c_dp, _c_dp]),
     "bgp_panel_trsm_inv": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
+    "bgp_ipc_alloc": (_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),
+    "bgp_ipc_open": (_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bgp_ipc_close": (_int, [ctypes.c_void_p, _c_dp]),
+    "bgp_ipc_free": (_int, [ctypes.c_void_p, _c_dp]),
+    "bgp_panel_trsm_push": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, ctypes.POINTER(ctypes.c_void_p),
+                                   _int, _i64, _i64, _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update_limited": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _int, _c_dp]),

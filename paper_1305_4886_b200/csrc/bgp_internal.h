@@ -141,7 +141,15 @@ struct GemmProblem {
   double* linv;
   int diag_need;
   double* cbase;       // set by launch_gemm: C tiles (register epilogue variant)
+  // GEMM_TRSM_PANEL push (multi-GPU): the epilogue also stores every solved
+  // block into tile (cTile - panel0) of each of npush destination panel
+  // buffers (this GPU's and its peers', IPC-mapped over NVLink); host-side
+  // bases, each holding push_tiles tiles, turned into tensor maps at launch
+  int npush;
+  double* const* push_dst;
+  int64_t push_tiles;
 };
+constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv = nullptr);
 

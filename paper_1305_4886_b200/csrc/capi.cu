@@ -722,6 +722,64 @@ int bgp_panel_trsm_inv(bgp_ctx_t ctx, const double* linv, double* A, int64_t cou
   return launch_gemm(ctx, p, A, A, count, A, count, count, (cudaStream_t)stream, linv);
 }
 
+int bgp_ipc_alloc(bgp_ctx_t ctx, size_t bytes, void** ptr, void* handle) {
+  if (!ctx || !ptr || !handle || bytes == 0) return BGP_E_ARG;
+  static_assert(sizeof(cudaIpcMemHandle_t) == BGP_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) return set_err(ctx, "ipc alloc", e);
+  e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return set_err(ctx, "ipc export", e);
+  }
+  return BGP_OK;
+}
+
+int bgp_ipc_open(bgp_ctx_t ctx, const void* handle, void** ptr) {
+  if (!ctx || !ptr || !handle) return BGP_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? BGP_OK : set_err(ctx, "ipc open", e);
+}
+
+int bgp_ipc_close(bgp_ctx_t ctx, void* ptr) {
+  if (!ctx) return BGP_E_ARG;
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? BGP_OK : set_err(ctx, "ipc close", e);
+}
+
+int bgp_ipc_free(bgp_ctx_t ctx, void* ptr) {
+  if (!ctx) return BGP_E_ARG;
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? BGP_OK : set_err(ctx, "ipc free", e);
+}
+
+int bgp_panel_trsm_push(bgp_ctx_t ctx, const double* linv, double* A, int64_t count, int tile,
+                        double* const* dst, int ndst, int64_t slot0, int64_t dst_tiles, void* stream) {
+  if (!valid_tile(tile) || count < 0 || ndst < 0 || ndst > BGP_MAX_PUSH || (ndst > 0 && !dst) || slot0 < 0 ||
+      slot0 + count > dst_tiles)
+    return BGP_E_ARG;
+  if (count == 0) return BGP_OK;
+  double* bases[BGP_MAX_PUSH];
+  for (int d = 0; d < ndst; ++d) bases[d] = dst[d] + slot0 * (int64_t)tile * tile;
+  GemmProblem p{};
+  p.mode = GEMM_TRSM_PANEL;
+  p.b = tile;
+  p.count = count;
+  p.panel0 = 0;
+  p.alpha = 1.0;
+  p.beta = 0.0;
+  p.check_info = true;
+  p.npush = ndst;
+  p.push_dst = bases;
+  p.push_tiles = dst_tiles - slot0;
+  return launch_gemm(ctx, p, A, A, count, A, count, count, (cudaStream_t)stream, linv);
+}
+
 int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, int tile, void* stream) {
   if (!valid_tile(tile)) return BGP_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

@@ -32,6 +32,7 @@
 
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 // Compiled twice: here with the BK = 16 configuration (namespace bgp::bk16)
 // and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks per tile.
@@ -323,6 +324,11 @@ __device__ __forceinline__ uint32_t lane_off(int p, int t, int q, int s4) {
   return (uint32_t)(k * 128 + ((((p << 2) ^ ((q >> 1) ^ k)) & 7) << 4) + ((q & 1) << 3));
 }
 
+// tensor maps of the panel push destinations (GEMM_TRSM_PANEL, npush > 0)
+struct PushMaps {
+  CUtensorMap map[BGP_MAX_PUSH];
+};
+
 // What the consumers need of a block, decoded once by the producer and
 // handed over with the block's first stage (written before the `full` arrive)
 struct BlockSlot {
@@ -541,7 +547,7 @@ __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ]
 
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p,
-                                              uint64_t* stagger) {
+                                              uint64_t* stagger, const PushMaps* pm) {
   static_assert((MI == 8 || MI == 4) && NJ == 4 && WN / 16 == 2, "load_frag: 64x32 or 32x32 warp tiles");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
@@ -743,9 +749,14 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         const int r0 = it.mrow0 + wm * WM + r * EPI_ROWS, c0 = it.nrow0 + wn * WN;
 #pragma unroll
         for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
-          if (it.store)
+          if (it.store) {
             tma_store_3d(tmC, wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
-          else
+            // fused panel push: the same box into every destination panel
+            // buffer (peer memory over NVLink), from the same staged rows
+            for (int d = 0; d < p.npush; ++d)
+              tma_store_3d(&pm->map[d], wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)(it.cTile - p.panel0),
+                           pol_stream);
+          } else
             tma_reduce_add_3d(tmC, wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
         }
         tma_store_commit();
@@ -781,12 +792,14 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   if (stagger_arrive && lane == 0) mbar_arrive(stagger);
   release_held();
   if (lane == 0 && store_pending) tma_store_wait_all0();
+  if (p.npush > 0) __threadfence_system();  // pushed panel visible to the peers
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmC,
-                     const GemmProblem p, unsigned long long* __restrict__ info) {
+                     const GemmProblem p, unsigned long long* __restrict__ info,
+                     const __grid_constant__ PushMaps pm) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int s_go;
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
@@ -843,7 +856,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #ifdef BGP_EXP_ONE_GROUP
     if (g != 0) return;
 #endif
-    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem));
+    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm);
   }
 }
 
@@ -891,6 +904,12 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mL, Linv ? Linv : Bbase, p.b, Linv ? 1 : nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
+  PushMaps pm;
+  memset(&pm, 0, sizeof(pm));
+  if (p.npush < 0 || p.npush > BGP_MAX_PUSH || (p.npush > 0 && p.mode != GEMM_TRSM_PANEL))
+    return set_err(ctx, "gemm: bad push destinations", cudaErrorInvalidValue);
+  for (int d = 0; d < p.npush; ++d)
+    if ((rc = make_tile_map(ctx, &pm.map[d], p.push_dst[d], p.b, p.push_tiles, 16, WN, true)) != BGP_OK) return rc;
   prepare();
   const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
   int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
@@ -904,7 +923,7 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
     }
   }
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
-                                                                  p.check_info ? ctx->d_info : nullptr);
+                                                                  p.check_info ? ctx->d_info : nullptr, pm);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");
 }

@@ -155,9 +155,16 @@ def dist_cholesky(dist, local, ops, comm):
         rest_items.append(it[cols != J + 1])
     dev_col = ops.prepare_items(col_items)
     dev_rest = ops.prepare_items(rest_items)
+    # fused panel exchange (TRSM epilogue stores into every rank's panel
+    # buffer over NVLink), or None: TRSM then NCCL broadcasts
+    xchg = ops.panel_exchange(comm, T) if hasattr(ops, "panel_exchange") else None
 
     def factor_panel(K):
         d = dist.owner(K, K)
+        if xchg is not None and K + 1 < T:
+            # every rank is done with buffer K % 2 (its last reader, step K-2's
+            # update, precedes this point on every rank's streams)
+            comm.barrier_stream()
         if me == d:
             info[0] = info[0] or ops.potrf_factor(local, dist.local[(K, K)], K * b,
                                                   inv_buf if K + 1 < T else None)
@@ -165,9 +172,16 @@ def dist_cholesky(dist, local, ops, comm):
             return
         comm.broadcast(inv_buf, d)
         s, c = dist.my_panel(K)
+        chunks, _, ntot = layouts[K]
+        if xchg is not None:
+            if c:
+                off = next(o for root, o, cnt in chunks if root == me and cnt)
+                xchg.push(inv_buf, local, s, c, K % 2, off)
+            comm.barrier_stream()  # panel K is in every rank's buffer
+            panels[K % 2] = xchg.bufs[K % 2]
+            return
         if c:
             ops.trsm_inv(inv_buf, local, s, c)
-        chunks, _, ntot = layouts[K]
         if panels[K % 2] is None or panels[K % 2].shape[0] < ntot:
             panels[K % 2] = ops.empty((max(ntot, 1), b, b))
         panel = panels[K % 2]
@@ -353,6 +367,31 @@ class TorchComm:
         self.dist.all_gather(outs, host, group=self.group)
         return [o.to(t.device) for o in outs]
 
+    def barrier_stream(self):
+        """A barrier ordered on the current stream (a 1-element all-reduce):
+        later work on this stream runs after every rank's earlier work."""
+        if self.world > 1:
+            import torch
+            nccl = self.dist.get_backend(self.group) == "nccl"
+            if getattr(self, "_one", None) is None:
+                dev = torch.cuda.current_device() if nccl else "cpu"
+                self._one = torch.ones(1, dtype=torch.int32, device=dev)
+            if not nccl and torch.cuda.is_available():
+                # host-side collective: finish this rank's queued GPU work first
+                torch.cuda.current_stream().synchronize()
+            if self.timeline is not None:
+                with self.timeline.span("comm"):
+                    self.dist.all_reduce(self._one, group=self.group)
+            else:
+                self.dist.all_reduce(self._one, group=self.group)
+
+    def all_gather_bytes(self, value):
+        if self.world == 1:
+            return [value]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, bytes(value), group=self.group)
+        return out
+
     def all_gather_float(self, value):
         if self.world == 1:
             return [value]
@@ -367,6 +406,102 @@ class TorchComm:
         self.dist.all_gather_object(vals, int(info), group=self.group)
         nz = [v for v in vals if v]
         return min(nz) if nz else 0
+
+
+class _DevMem:
+    """Zero-copy torch view of a raw device allocation."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3}
+
+
+class PanelExchange:
+    """Two panel buffers per rank in IPC-exported device memory, opened by
+    every peer: the panel TRSM stores each solved tile straight into all
+    ranks' buffers (bgp_panel_trsm_push), so the solve and the panel
+    exchange are one kernel over NVLink peer memory instead of a TRSM
+    followed by NCCL broadcasts.  Built collectively; `ok` is False (and the
+    schedule falls back to NCCL broadcasts) when the peer mappings or a
+    one-tile self-check fail on any rank."""
+
+    def __init__(self, cluster, comm, tiles):
+        import ctypes
+
+        import torch
+        self.cl, self.comm = cluster, comm
+        b = cluster.tile
+        self.tiles = max(tiles, comm.world)
+        nbytes = self.tiles * b * b * 8
+        self.own, self.peers = [], []
+        self.bufs, self.dst = [], []
+        ok = True
+        try:
+            for _ in range(2):
+                ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+                cluster.call("bgp_ipc_alloc", nbytes, ctypes.byref(ptr), h)
+                self.own.append(ptr.value)
+                handles = comm.all_gather_bytes(h.raw)
+                ptrs = []
+                for r, hr in enumerate(handles):
+                    if r == comm_rank(comm):
+                        ptrs.append(ptr.value)
+                        continue
+                    q = ctypes.c_void_p()
+                    cluster.call("bgp_ipc_open", hr, ctypes.byref(q))
+                    self.peers.append(q.value)
+                    ptrs.append(q.value)
+                self.dst.append((ctypes.c_void_p * len(ptrs))(*ptrs))
+                self.bufs.append(torch.as_tensor(_DevMem(ptr.value, self.tiles * b * b),
+                                                 device=cluster.device).view(self.tiles, b, b))
+        except Exception:
+            ok = False
+        self.ok = self._agree(ok and self._self_check())
+
+    def _agree(self, ok):
+        vals = self.comm.all_gather_bytes(b"\x01" if ok else b"\x00")
+        return all(v == b"\x01" for v in vals)
+
+    def _self_check(self):
+        """Every rank pushes a tile (identity inverse: the tile itself) into
+        slot `rank` of buffer 0 everywhere; each rank then checks its slots."""
+        import torch
+        try:
+            b, me, G = self.cl.tile, comm_rank(self.comm), self.comm.world
+            eye = torch.eye(b, dtype=torch.float64, device=self.cl.device)
+            t = torch.full((1, b, b), float(me + 1), dtype=torch.float64, device=self.cl.device)
+            self.comm.barrier_stream()
+            self.push(eye, t, 0, 1, 0, me)
+            self.comm.barrier_stream()
+            torch.cuda.synchronize(self.cl.device)
+            got = self.bufs[0][:G, 0, 0].cpu().tolist()
+            return got == [float(r + 1) for r in range(G)]
+        except Exception:
+            return False
+
+    def push(self, inv, local, start, count, which, slot0):
+        import ctypes
+        self.cl.call("bgp_panel_trsm_push", ctypes.c_void_p(inv.data_ptr()),
+                     ctypes.c_void_p(local[start].data_ptr()), count, self.cl.tile,
+                     self.dst[which], len(self.dst[which]), slot0, self.tiles, self.cl.stream)
+
+    def close(self):
+        for q in self.peers:
+            self.cl.lib.bgp_ipc_close(self.cl._ctx, q)
+        self.peers = []
+        try:
+            self.comm.barrier_stream()
+            import torch
+            torch.cuda.synchronize(self.cl.device)
+        except Exception:
+            pass
+        for q in self.own:
+            self.cl.lib.bgp_ipc_free(self.cl._ctx, q)
+        self.own, self.bufs = [], []
+
+
+def comm_rank(comm):
+    return comm.dist.get_rank(comm.group) if comm.world > 1 else 0
 
 
 class LibTileOps:
@@ -444,6 +579,22 @@ class LibTileOps:
             out.append((dev[4 * off:4 * (off + len(a))], len(a)))
             off += len(a)
         return out
+
+    def panel_exchange(self, comm, T):
+        """The cluster's PanelExchange for T panel tiles (built collectively
+        on first use), or None for NCCL broadcasts (BGP_PANEL_XFER=nccl, one
+        rank, or a failed self-check)."""
+        import os
+        if comm.world == 1 or os.environ.get("BGP_PANEL_XFER", "push") != "push":
+            return None
+        cache = self.cl.__dict__.setdefault("_panel_xchg", {})
+        x = cache.get("x")
+        if x is None or x.tiles < T:
+            if x is not None:
+                x.close()
+            x = PanelExchange(self.cl, comm, T)
+            cache["x"] = x
+        return x if x.ok else None
 
     # SMs left free during a reserved update for the side stream's NCCL
     # collectives, POTRF and panel solve

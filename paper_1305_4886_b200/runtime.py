@@ -231,6 +231,9 @@ class B200Cluster:
             self.store.clear()
             self._dev_inputs.clear()
             try:
+                x = self.__dict__.get("_panel_xchg", {}).get("x")
+                if x is not None:  # peer panel mappings (collective)
+                    x.close()
                 _torch().cuda.synchronize(self.device)
             finally:
                 self.lib.bgp_finalize(self._ctx)

@@ -29,10 +29,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, xfer="push"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
-                      RANK=str(rank), LOCAL_RANK="0")
+                      RANK=str(rank), LOCAL_RANK="0", BGP_PANEL_XFER=xfer)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import blockgp_oracle as orc
@@ -50,6 +50,8 @@ def _worker(rank, world, port, q):
         L, stats = distla.distributed_cholesky(cl, C, "L")
         cl.comm_timeline = False
         out["comm"] = cl.last_comm
+        x = cl.__dict__.get("_panel_xchg", {}).get("x")
+        out["xfer"] = "push" if (x is not None and x.ok) else "nccl"
         out["L"] = distla.collect(cl, L)
         bvec = np.random.default_rng(5).standard_normal(n)
         bd = distla.distribute(cl, "b", bvec, "vector", lay)
@@ -80,14 +82,17 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_multi_rank_path_on_one_gpu(world):
+@pytest.mark.parametrize("world,xfer", [(2, "push"), (4, "push"), (2, "nccl")])
+def test_multi_rank_path_on_one_gpu(world, xfer):
+    """xfer "push": the panel TRSM stores into every rank's IPC-mapped panel
+    buffer (bgp_panel_trsm_push; here all mappings are on cuda:0); "nccl":
+    TRSM, then broadcasts of the panel chunks."""
     import torch.multiprocessing as mp
     from oracle import blockgp_oracle as orc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, xfer)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -123,6 +128,7 @@ def test_multi_rank_path_on_one_gpu(world):
         assert relerr(r["x"], np.linalg.solve(A, bvec)) <= 1e-10
         assert abs(r["logdet"] - np.linalg.slogdet(A)[1]) <= 1e-12 * abs(r["logdet"])
         assert r["npd"] == 1 and "Ln" not in r["ls"] and "Cn" not in r["ls"]
+        assert r["xfer"] == xfer
         c = r["comm"]
         assert c["collectives"] > 0 and 0.0 <= c["exposed_comm_ms"] <= c["comm_ms"] + 1e-6
         assert abs(r["ll"] - want_ll) <= 1e-10 * abs(want_ll)
