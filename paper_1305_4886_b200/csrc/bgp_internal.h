@@ -86,6 +86,8 @@ void potrf_prepare();
 void gemm_block_counts(int b, int* tile_need, int* diag_need, int* groups_per_cta);
 size_t potrf_smem_bytes(int b);
 size_t tri_inv_smem_bytes();
+// tile POTRF (+ inverse) with the tile staged in shared memory for b <= 128
+size_t tile_potrf_inv_smem_bytes(int b, bool inv);
 
 // tile kernels
 // info value reserved for a look-ahead wait that never completed (a bug, not data)

@@ -842,9 +842,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         double* psm = reinterpret_cast<double*>(smem);
         if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
         named_bar_sync(2, 256);
-        if (s_go && tile_potrf_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info, psm, ctid, 2) &&
+        if (s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
+                                          p.trsm_next ? p.linv : nullptr, psm, ctid, 2) &&
             p.trsm_next) {
-          tri_inv_diag_device(p.potrf_tile, p.dinv, p.b, p.linv, psm, ctid, 2);
           __threadfence();
           named_bar_sync(2, 256);
           if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);
@@ -917,7 +917,7 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   if (p.potrf_tile) {
     static bool attr = false;
     if (!attr) {  // the look-ahead CTA's device POTRF / inverse must fit the ring memory
-      if (potrf_smem_bytes(p.b) > (size_t)(GROUPS * GROUP_BYTES) || tri_inv_smem_bytes() > (size_t)(GROUPS * GROUP_BYTES))
+      if (tile_potrf_inv_smem_bytes(p.b, true) > (size_t)(GROUPS * GROUP_BYTES))
         return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
       attr = true;
     }

@@ -279,6 +279,7 @@ constexpr int TINV_THREADS = 256;
 // acc (32x32 block as 4x4 8x8 DMMA tiles) += A(32x32) B(32x32): A(r, k) at
 // a[k * lda + r], B(k, c) at bm[c * ldb + k] (both column-major, from L2);
 // all 64 fragments of a k range are loaded before the 128 DMMAs.
+template <bool ASMEM>
 __device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double* __restrict__ a, int64_t lda,
                                             const double* __restrict__ bm, int64_t ldb, int lane) {
   const int q = lane >> 2, s4 = lane & 3;
@@ -290,7 +291,7 @@ __device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int kk = kh * 16 + 4 * k + s4;
-        av[k][t] = __ldcg(a + (int64_t)kk * lda + t * 8 + q);
+        av[k][t] = ASMEM ? a[(int64_t)kk * lda + t * 8 + q] : __ldcg(a + (int64_t)kk * lda + t * 8 + q);
         bv[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * ldb + kk);
       }
 #pragma unroll
@@ -309,6 +310,8 @@ __device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double
 // and only needs diagonals < d, so all blocks of a diagonal are independent:
 // one warp per 32x32 block, 4x4 DMMA tiles, 64 fragment loads (L2: the tile
 // was just factored) in flight per 128 DMMAs.
+// LSMEM: L is a shared-memory copy of the tile (ld b), see tile_potrf_inv_device.
+template <bool LSMEM = false>
 static __device__ __noinline__ void tri_inv_diag_device(const double* __restrict__ L, const double* __restrict__ dinv, int b,
                                     double* __restrict__ Linv, double* S, int tid, int bar) {
   // S: per warp one 32x32 partial sum, [(w*32 + r)*33 + c]
@@ -336,7 +339,8 @@ static __device__ __noinline__ void tri_inv_diag_device(const double* __restrict
         for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
       // S = sum_m L[i][m] Linv[m][j]
       for (int m = j; m < i; ++m)
-        block_mma32(acc, L + (int64_t)(m * NB) * b + i * NB, b, Linv + (int64_t)(j * NB) * b + m * NB, b, lane);
+        block_mma32<LSMEM>(acc, L + (int64_t)(m * NB) * b + i * NB, b, Linv + (int64_t)(j * NB) * b + m * NB, b,
+                           lane);
 #pragma unroll
       for (int tr = 0; tr < 4; ++tr)
 #pragma unroll
@@ -376,5 +380,49 @@ static __device__ __noinline__ void tri_inv_diag_device(const double* __restrict
   }
 }
 
+
+// Tiles up to SMEM_TILE: the whole b x b tile is copied into shared memory,
+// factored there (no L2 round trip between the sub-panel steps) and, with
+// Linv, inverted from the shared copy; L goes back once at the end.  The
+// dependent chain of small steps is what bounds these tiles (tail steps,
+// small problems).  Larger tiles run in place through L2.  `sm` holds
+// tile_potrf_inv_smem_bytes(b).
+constexpr int SMEM_TILE = 128;
+
+static __device__ __noinline__ bool tile_potrf_inv_device(double* __restrict__ A, int b, int64_t row0,
+                                                          double* __restrict__ dinv,
+                                                          unsigned long long* __restrict__ info,
+                                                          double* __restrict__ Linv, double* sm, int tid, int bar) {
+  static_assert(POTRF_THREADS == TINV_THREADS, "one thread set");
+  if (b > SMEM_TILE) {
+    const bool ok = tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar);
+    if (ok && Linv) {
+      __threadfence_block();
+      named_bar_sync(bar, POTRF_THREADS);
+      tri_inv_diag_device<false>(A, dinv, b, Linv, sm, tid, bar);
+    }
+    return ok;
+  }
+  double* T = sm;
+  double* scratch = sm + (size_t)b * b;
+  const int n2 = b * b / 2;
+  const double2* src = reinterpret_cast<const double2*>(A);
+  double2* dst = reinterpret_cast<double2*>(T);
+  for (int i = tid; i < n2; i += POTRF_THREADS) dst[i] = __ldcg(src + i);
+  named_bar_sync(bar, POTRF_THREADS);
+  const bool ok = tile_potrf_device(T, b, row0, dinv, info, scratch, tid, bar);
+  if (ok && Linv) {
+    __threadfence_block();
+    named_bar_sync(bar, POTRF_THREADS);
+    tri_inv_diag_device<true>(T, dinv, b, Linv, scratch, tid, bar);
+  }
+  named_bar_sync(bar, POTRF_THREADS);
+  double2* out = reinterpret_cast<double2*>(A);
+  const double2* Ts = reinterpret_cast<const double2*>(T);
+  for (int i = tid; i < n2; i += POTRF_THREADS) out[i] = Ts[i];
+  __threadfence();
+  named_bar_sync(bar, POTRF_THREADS);
+  return ok;
+}
 
 }  // namespace bgp

@@ -19,6 +19,12 @@
 namespace bgp {
 
 size_t potrf_smem_bytes(int b) { return (size_t)(2 * NB * 33 + (b - NB) * PLD + 2 * NB + 2) * sizeof(double); }
+size_t tri_inv_smem_bytes() { return (size_t)(TINV_THREADS / 32) * NB * 33 * sizeof(double); }
+size_t tile_potrf_inv_smem_bytes(int b, bool inv) {
+  size_t scratch = potrf_smem_bytes(b);
+  if (inv && tri_inv_smem_bytes() > scratch) scratch = tri_inv_smem_bytes();
+  return (b <= SMEM_TILE ? (size_t)b * b * sizeof(double) : 0) + scratch;
+}
 
 __global__ void __launch_bounds__(POTRF_THREADS, 1)
     tile_potrf_kernel(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
@@ -51,7 +57,7 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   }
   __syncthreads();
   if (s_skip) return;
-  tile_potrf_device(A, b, row0, dinv, info, sm, tid, 0);
+  tile_potrf_inv_device(A, b, row0, dinv, info, nullptr, sm, tid, 0);
 }
 
 
@@ -62,13 +68,11 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
 // and only needs diagonals < d, so all blocks of a diagonal are independent.
 // Both products run on DMMA with fragments loaded from L2 (the tile was just
 // factored); the partial sums of a diagonal are staged in shared memory.
-size_t tri_inv_smem_bytes() { return (size_t)(TINV_THREADS / 32) * NB * 33 * sizeof(double); }
-
 __global__ void __launch_bounds__(TINV_THREADS, 1)
     tri_inv_diag_kernel(const double* __restrict__ L, const double* __restrict__ dinv, int b,
                         double* __restrict__ Linv, int* __restrict__ done) {
   extern __shared__ double S[];
-  tri_inv_diag_device(L, dinv, b, Linv, S, threadIdx.x, 0);
+  tri_inv_diag_device<false>(L, dinv, b, Linv, S, threadIdx.x, 0);
   if (done) {  // publish: the fused panel TRSM of the trailing update waits for this
     __threadfence();
     __syncthreads();
@@ -196,7 +200,7 @@ void potrf_prepare() {
 
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
                       const int* gate, int gate_need) {
-  const size_t smem = potrf_smem_bytes(b);
+  const size_t smem = tile_potrf_inv_smem_bytes(b, false);
   potrf_prepare();
   tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info, gate, gate_need);
   ctx->launches++;

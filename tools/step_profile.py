@@ -30,7 +30,7 @@ if args.config == 4:
     spec, theta = builtin_spec("matern-nugget", X, nu=0.5), np.array([1.0, 0.08, 0.02])
 else:
     from oracle.blockgp_oracle import config_inputs
-    kern, X, theta, extra, z = config_inputs(2)
+    kern, X, theta, extra, z = config_inputs(args.config)
     spec = builtin_spec(kern, X, **extra)
     y = np.random.default_rng(0).standard_normal(len(X))  # timing only
 prob = KrigeProblem(cl, "p", spec, y, theta)
