@@ -35,7 +35,8 @@
 #include <string.h>
 
 // Compiled twice: here with the BK = 16 configuration (namespace bgp::bk16)
-// and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks per tile.
+// and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks bk32
+// unless BGP_GEMM_CFG=16.
 #ifndef BGP_GEMM_NS
 #define BGP_GEMM_NS bk16
 #endif
@@ -48,9 +49,12 @@ namespace BGP_GEMM_NS {
 //        (setmaxnreg.dec to PRODUCER_REGS);
 //   WG1, WG2  consumers: 4 MMA warps each (2 x 2 warps of 64x32), each group
 //        owns a 128x64 output block at a time (setmaxnreg.inc to CONSUMER_REGS).
-// The two consumer groups take alternate blocks of the CTA's static schedule
-// and run concurrently, so one group's epilogue overlaps the other group's
-// main loop and the DMMA pipe never drains between blocks.
+// Each group's producer claims blocks from the launch's task queue, and the
+// two groups run concurrently (half a block apart), so one group's epilogue
+// overlaps the other group's main loop and the DMMA pipe never drains.
+// Compiled twice (see below): BK = 32 is the production configuration at
+// every tile size, BK = 16 a diagnostic (BGP_GEMM_CFG=16); the other
+// BGP_GEMM_* / BGP_EXP_* macros select probe builds (tools/gemm_probe.sh).
 #if defined(BGP_GEMM_3G)  // three consumer groups of 2x2 warps of 32x32: 64x64 blocks
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 16;
 constexpr int GROUPS = 3;
@@ -608,11 +612,13 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // Software pipeline over the stage ring.  A stage holds four k4
-    // half-steps (h0..h3); fragments alternate between two register sets, so
-    // the loads of half-step h+1 issue in the DMMA gaps of half-step h.  The
-    // wait for stage s+1 sits before the last half-step of stage s, and
-    // stage s is released once its last DMMA issued (fragments in registers).
+    // Software pipeline over the stage ring.  A stage holds BK / 4 k4
+    // half-steps; fragments alternate between two register sets, so the
+    // loads of half-step h+1 issue in the DMMA gaps of half-step h.  The wait
+    // for stage s+1 sits before the last half-step of stage s, and stage s
+    // is released once its last DMMA issued (fragments in registers) -- except
+    // the block's last stage under EPI_IN_STAGE, which holds epilogue rows
+    // until release_held() early in the next block.
 #ifdef BGP_EXP_TRACE
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][0] = clock64();
