@@ -379,11 +379,12 @@ class TorchComm:
             if not nccl and torch.cuda.is_available():
                 # host-side collective: finish this rank's queued GPU work first
                 torch.cuda.current_stream().synchronize()
+            op = self.dist.ReduceOp.MAX  # the value stays 1
             if self.timeline is not None:
                 with self.timeline.span("comm"):
-                    self.dist.all_reduce(self._one, group=self.group)
+                    self.dist.all_reduce(self._one, op=op, group=self.group)
             else:
-                self.dist.all_reduce(self._one, group=self.group)
+                self.dist.all_reduce(self._one, op=op, group=self.group)
 
     def all_gather_bytes(self, value):
         if self.world == 1:
