@@ -427,25 +427,37 @@ class PanelExchange:
     one-tile self-check fail on any rank."""
 
     def __init__(self, cluster, comm, tiles):
+        # Every rank runs the same sequence of collectives whatever fails
+        # locally (a rank that stops early would leave the others waiting).
         import ctypes
+        import warnings
 
         import torch
         self.cl, self.comm = cluster, comm
         b = cluster.tile
         self.tiles = max(tiles, comm.world)
         nbytes = self.tiles * b * b * 8
+        me = comm_rank(comm)
         self.own, self.peers = [], []
         self.bufs, self.dst = [], []
-        ok = True
-        try:
-            for _ in range(2):
-                ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
-                cluster.call("bgp_ipc_alloc", nbytes, ctypes.byref(ptr), h)
-                self.own.append(ptr.value)
-                handles = comm.all_gather_bytes(h.raw)
+        ok, why = True, None
+        for _ in range(2):
+            ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            if ok:
+                try:
+                    cluster.call("bgp_ipc_alloc", nbytes, ctypes.byref(ptr), h)
+                    self.own.append(ptr.value)
+                except Exception as exc:
+                    ok, why = False, exc
+            handles = comm.all_gather_bytes(h.raw if ok else b"")
+            if ok and any(len(hr) != 64 for hr in handles):
+                ok, why = False, "a peer could not export its buffer"
+            if not ok:
+                continue
+            try:
                 ptrs = []
                 for r, hr in enumerate(handles):
-                    if r == comm_rank(comm):
+                    if r == me:
                         ptrs.append(ptr.value)
                         continue
                     q = ctypes.c_void_p()
@@ -455,11 +467,14 @@ class PanelExchange:
                 self.dst.append((ctypes.c_void_p * len(ptrs))(*ptrs))
                 self.bufs.append(torch.as_tensor(_DevMem(ptr.value, self.tiles * b * b),
                                                  device=cluster.device).view(self.tiles, b, b))
-        except Exception as exc:  # no P2P mapping: the schedule keeps NCCL broadcasts
-            import warnings
-            warnings.warn(f"panel push unavailable ({exc}); using NCCL panel broadcasts")
-            ok = False
-        self.ok = self._agree(ok and self._self_check())
+            except Exception as exc:
+                ok, why = False, exc
+        if not self._agree(ok):  # no P2P mapping somewhere: NCCL broadcasts
+            if why is not None:
+                warnings.warn(f"panel push unavailable ({why}); using NCCL panel broadcasts")
+            self.ok = False
+            return
+        self.ok = self._agree(self._self_check())
 
     def _agree(self, ok):
         vals = self.comm.all_gather_bytes(b"\x01" if ok else b"\x00")
@@ -467,26 +482,33 @@ class PanelExchange:
 
     def _self_check(self):
         """Every rank pushes a tile (identity inverse: the tile itself) into
-        slot `rank` of buffer 0 everywhere; each rank then checks its slots."""
+        slot `rank` of buffer 0 everywhere; each rank then checks its slots.
+        The two barriers run on every rank even if the push raises."""
+        import warnings
+
         import torch
+        b, me, G = self.cl.tile, comm_rank(self.comm), self.comm.world
+        err = None
+        self.comm.barrier_stream()
         try:
-            b, me, G = self.cl.tile, comm_rank(self.comm), self.comm.world
             eye = torch.eye(b, dtype=torch.float64, device=self.cl.device)
             t = torch.full((1, b, b), float(me + 1), dtype=torch.float64, device=self.cl.device)
-            self.comm.barrier_stream()
             self.push(eye, t, 0, 1, 0, me)
-            self.comm.barrier_stream()
-            torch.cuda.synchronize(self.cl.device)
-            got = self.bufs[0][:G, 0, 0].cpu().tolist()
-            if got != [float(r + 1) for r in range(G)]:
-                import warnings
-                warnings.warn(f"panel push self-check failed (got {got}); using NCCL panel broadcasts")
-                return False
-            return True
         except Exception as exc:
-            import warnings
-            warnings.warn(f"panel push self-check failed ({exc}); using NCCL panel broadcasts")
+            err = exc
+        self.comm.barrier_stream()
+        if err is None:
+            try:
+                torch.cuda.synchronize(self.cl.device)
+                got = self.bufs[0][:G, 0, 0].cpu().tolist()
+                if got != [float(r + 1) for r in range(G)]:
+                    err = f"received {got}"
+            except Exception as exc:
+                err = exc
+        if err is not None:
+            warnings.warn(f"panel push self-check failed ({err}); using NCCL panel broadcasts")
             return False
+        return True
 
     def push(self, inv, local, start, count, which, slot0):
         import ctypes
