@@ -41,6 +41,8 @@ struct Ctx {
   size_t gate_cap = 0;
   double* d_linv = nullptr;  // inverse of the current diagonal tile (panel TRSM on DMMA)
   size_t linv_cap = 0;
+  double* d_linv_all = nullptr;  // inverses of every diagonal tile (kriging solve)
+  size_t linv_all_cap = 0;
   int* d_queue = nullptr;  // task counter of standalone GEMM launches
   size_t queue_cap = 0;
   double* d_tail[2] = {nullptr, nullptr};  // re-tiled trailing triangles of the Cholesky tail
@@ -98,6 +100,9 @@ int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv,
 int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
                    int* done = nullptr);
 int launch_diag_inv(Ctx* ctx, const double* L, int T, int b, int64_t n, double* dinv, cudaStream_t s);
+// inverses of all T diagonal tiles of a factored packed triangle (dinv from launch_diag_inv)
+int launch_tri_inv_batch(Ctx* ctx, const double* L, int T, const double* dinv, int b, double* Linv,
+                         cudaStream_t s);
 int launch_panel_trsm(Ctx* ctx, const double* Ld, const double* dinv, double* A, int64_t count, int b,
                       int trans, cudaStream_t s, bool check_info = true);
 
@@ -150,6 +155,10 @@ struct GemmProblem {
   int npush;
   double* const* push_dst;
   int64_t push_tiles;
+  // GEMM_TRSM_PANEL out of place: C (the launch's Cbase) is a separate
+  // buffer, so the column passes of a slab read only A and are independent
+  // tasks (in place they must run right to left in one task)
+  int trsm_oop;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
@@ -173,6 +182,7 @@ int launch_unpack(Ctx* ctx, int kind, const double* tiles, int64_t nrow, int64_t
                   double* dense, int64_t ld, cudaStream_t s);
 int launch_tri_diagonal(Ctx* ctx, const double* L, int64_t n, int b, double* d, cudaStream_t s);
 int launch_sub(Ctx* ctx, const double* a, const double* bb, double* out, int64_t count, cudaStream_t s);
+int launch_copy(Ctx* ctx, double* dst, const double* src, int64_t count, cudaStream_t s);
 
 }  // namespace bgp
 

@@ -170,6 +170,7 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_sync) cudaFree(ctx->d_sync);
   if (ctx->d_gate) cudaFree(ctx->d_gate);
   if (ctx->d_linv) cudaFree(ctx->d_linv);
+  if (ctx->d_linv_all) cudaFree(ctx->d_linv_all);
   for (int l = 0; l < 2; ++l)
     if (ctx->d_tail[l]) cudaFree(ctx->d_tail[l]);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
@@ -507,10 +508,29 @@ int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* B
   if ((rc = launch_diag_inv(ctx, L, T, b, n, ctx->d_dinv, s))) return rc;
   const int64_t tsz = (int64_t)b * b;
   const int64_t nL = tri_count(T), nV = (int64_t)Tm * T;
+  // every diagonal tile's inverse at once (T CTAs), so each panel step is a
+  // DMMA GEMM X_J = B_J Linv_J^T (in place, TRSM_PANEL mode)
+  // (T tiles of inverses followed by Tm tiles of panel scratch)
+  if ((rc = ensure(ctx, (void**)&ctx->d_linv_all, &ctx->linv_all_cap, (size_t)(T + Tm) * tsz * sizeof(double))))
+    return rc;
+  if ((rc = launch_tri_inv_batch(ctx, L, T, ctx->d_dinv, b, ctx->d_linv_all, s))) return rc;
+  double* xs = ctx->d_linv_all + (int64_t)T * tsz;
   for (int J = 0; J < T; ++J) {
-    const double* ljj = L + tri_index(J, J, T) * tsz;
-    if ((rc = launch_panel_trsm(ctx, ljj, ctx->d_dinv + per_tile * J, Bt + (int64_t)J * Tm * tsz, Tm, b, 0, s)))
+    // X_J = B_J Linv_J^T into the scratch panel (all column passes
+    // independent: one wave), then back over B_J for the GEMM and the result
+    GemmProblem pt{};
+    pt.mode = GEMM_TRSM_PANEL;
+    pt.b = b;
+    pt.count = Tm;
+    pt.panel0 = 0;
+    pt.alpha = 1.0;
+    pt.beta = 0.0;
+    pt.check_info = true;
+    pt.trsm_oop = 1;
+    double* panel = Bt + (int64_t)J * Tm * tsz;
+    if ((rc = launch_gemm(ctx, pt, xs, panel, Tm, panel, Tm, Tm, s, ctx->d_linv_all + (int64_t)J * tsz)))
       return rc;
+    if ((rc = launch_copy(ctx, panel, xs, (int64_t)Tm * tsz, s))) return rc;
     if (J + 1 < T) {
       GemmProblem p{};
       p.mode = GEMM_RECT_TRAIL;

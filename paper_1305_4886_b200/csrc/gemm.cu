@@ -153,7 +153,7 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
 // b/64 column blocks right to left, so the in-place solve never overwrites
 // columns a later block still reads.
 __host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p) {
-  if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM);
+  if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM) * (p.trsm_oop ? p.b / BN : 1);
   if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next) return (int64_t)(p.T - p.J - 2) * (p.b / BM);
   return 0;
 }
@@ -237,6 +237,10 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   int64_t idx;
   if (gemm_task_kind(p, task, idx)) {
     // standalone panel, or the fused TRSM of panel J+1 (tiles J+2 .. T-1)
+    if (p.mode == GEMM_TRSM_PANEL && p.trsm_oop) {  // one independent pass per task
+      pass = (int)(idx % nbn);
+      idx /= nbn;
+    }
     trsm_block(it, p, idx, pass, p.mode == GEMM_TRSM_PANEL ? p.panel0 : tri_index(p.J + 2, p.J + 1, p.T));
     return it;
   }
@@ -301,7 +305,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
-  return gemm_task_kind(p, task, idx) ? p.b / BN : 1;
+  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop)) ? p.b / BN : 1;
 }
 
 // spin (acquire, exponential back-off, bounded) until *flag >= need or the

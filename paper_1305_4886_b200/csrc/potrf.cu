@@ -80,6 +80,27 @@ __global__ void __launch_bounds__(TINV_THREADS, 1)
   }
 }
 
+// Inverses of all T diagonal tiles of a factored packed triangle, one CTA
+// per tile (the kriging solve's panel steps then run on the DMMA GEMM as
+// X = B Linv^T instead of a substitution kernel on the serial path).
+__global__ void __launch_bounds__(TINV_THREADS, 1)
+    tri_inv_batch_kernel(const double* __restrict__ L, int T, const double* __restrict__ dinv, int b,
+                         double* __restrict__ Linv, const unsigned long long* __restrict__ info) {
+  extern __shared__ double S[];
+  if (info && *(volatile const unsigned long long*)info != 0ull) return;  // singular diagonal found
+  const int J = blockIdx.x;
+  const int64_t tsz = (int64_t)b * b;
+  tri_inv_diag_device<false>(L + tri_index(J, J, T) * tsz, dinv + (int64_t)J * (b / NB) * NB * NB, b,
+                             Linv + (int64_t)J * tsz, S, threadIdx.x, 0);
+}
+
+int launch_tri_inv_batch(Ctx* ctx, const double* L, int T, const double* dinv, int b, double* Linv,
+                         cudaStream_t s) {
+  tri_inv_batch_kernel<<<T, TINV_THREADS, tri_inv_smem_bytes(), s>>>(L, T, dinv, b, Linv, ctx->d_info);
+  ctx->launches++;
+  return check_launch(ctx, "tri_inv_batch");
+}
+
 // inverses of the 32x32 diagonal sub-blocks of every diagonal tile of a packed
 // triangle; zero diagonal -> info (SingularDiagonal, kernels.py:245-246)
 __global__ void diag_inv_kernel(const double* __restrict__ L, int T, int b, int64_t n,
@@ -192,6 +213,7 @@ void potrf_prepare() {
     cudaFuncSetAttribute(tile_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(tri_inv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, diag_inv_kernel);
     done = true;

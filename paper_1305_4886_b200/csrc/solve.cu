@@ -592,4 +592,25 @@ int launch_sub(Ctx* ctx, const double* a, const double* bb, double* out, int64_t
   return check_launch(ctx, "sub");
 }
 
+// dst = src for `count` doubles (count even, 16-byte aligned): an SM copy,
+// which is several times faster on the kriging solve's serial path than a
+// device-to-device cudaMemcpyAsync of a few MB
+__global__ void copy2_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int64_t n2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcs(src + i);
+}
+
+int launch_copy(Ctx* ctx, double* dst, const double* src, int64_t count, cudaStream_t s) {
+  if (count <= 0) return BGP_OK;
+  if ((count & 1) || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15))
+    return set_err(ctx, "copy: needs 16-byte aligned even counts", cudaErrorInvalidValue);
+  const int64_t n2 = count / 2;
+  int64_t blocks = (n2 + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 8) blocks = (int64_t)ctx->num_sms * 8;
+  copy2_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst),
+                                                n2);
+  ctx->launches++;
+  return check_launch(ctx, "copy");
+}
+
 }  // namespace bgp
