@@ -515,9 +515,9 @@ int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* B
     return rc;
   if ((rc = launch_tri_inv_batch(ctx, L, T, ctx->d_dinv, b, ctx->d_linv_all, s))) return rc;
   double* xs = ctx->d_linv_all + (int64_t)T * tsz;
-  for (int J = 0; J < T; ++J) {
-    // X_J = B_J Linv_J^T into the scratch panel (all column passes
-    // independent: one wave), then back over B_J for the GEMM and the result
+  // panel 0: X_0 = B_0 Linv_0^T out of place (all column passes independent,
+  // one wave), copied back over B_0
+  {
     GemmProblem pt{};
     pt.mode = GEMM_TRSM_PANEL;
     pt.b = b;
@@ -527,23 +527,39 @@ int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* B
     pt.beta = 0.0;
     pt.check_info = true;
     pt.trsm_oop = 1;
-    double* panel = Bt + (int64_t)J * Tm * tsz;
-    if ((rc = launch_gemm(ctx, pt, xs, panel, Tm, panel, Tm, Tm, s, ctx->d_linv_all + (int64_t)J * tsz)))
-      return rc;
-    if ((rc = launch_copy(ctx, panel, xs, (int64_t)Tm * tsz, s))) return rc;
-    if (J + 1 < T) {
-      GemmProblem p{};
-      p.mode = GEMM_RECT_TRAIL;
-      p.b = b;
-      p.T = T;
-      p.J = J;
-      p.Tm = Tm;
-      p.Tn = T;
-      p.alpha = -1.0;
-      p.beta = 1.0;
-      p.check_info = true;
-      if ((rc = launch_gemm(ctx, p, Bt, Bt, nV, L, nL, nV, s))) return rc;
-    }
+    if ((rc = launch_gemm(ctx, pt, xs, Bt, Tm, Bt, Tm, Tm, s, ctx->d_linv_all))) return rc;
+    if ((rc = launch_copy(ctx, Bt, xs, (int64_t)Tm * tsz, s))) return rc;
+  }
+  // step J: B_I -= X_J L_IJ^T for I > J, row block J+1 first; its solve
+  // X_{J+1} = B_{J+1} Linv_{J+1}^T runs in the same launch as gated tasks
+  // (in place, column passes right to left), so the serial panel solve is
+  // off the critical path
+  const int stride = (Tm + 2 + 1) & ~1;  // Tm tile counters + the 64-bit task counter
+  if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
+  {
+    cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
+    if (e != cudaSuccess) return set_err(ctx, "kriging solve counters", e);
+  }
+  int tile_need, diag_need, groups_per_cta;
+  gemm_block_counts(b, &tile_need, &diag_need, &groups_per_cta);
+  for (int J = 0; J + 1 < T; ++J) {
+    int* gate = ctx->d_gate + (int64_t)J * stride;
+    GemmProblem p{};
+    p.mode = GEMM_RECT_TRAIL;
+    p.b = b;
+    p.T = T;
+    p.J = J;
+    p.Tm = Tm;
+    p.Tn = T;
+    p.alpha = -1.0;
+    p.beta = 1.0;
+    p.check_info = true;
+    p.queue = gate + stride - 2;
+    p.col_gate = gate;
+    p.trsm_next = 1;
+    p.tile_need = tile_need;
+    p.trsm_tail = 2 * groups_per_cta * ctx->num_sms;
+    if ((rc = launch_gemm(ctx, p, Bt, Bt, nV, L, nL, nV, s, ctx->d_linv_all + (int64_t)(J + 1) * tsz))) return rc;
   }
   return read_info(ctx, s, info);
 }

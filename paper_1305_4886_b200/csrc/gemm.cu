@@ -155,7 +155,12 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
 __host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p) {
   if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM) * (p.trsm_oop ? p.b / BN : 1);
   if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next) return (int64_t)(p.T - p.J - 2) * (p.b / BM);
+  if (p.mode == GEMM_RECT_TRAIL && p.trsm_next) return (int64_t)p.Tm * (p.b / BM);
   return 0;
+}
+// a trailing update with the next panel's solve appended as gated tasks
+__host__ __device__ __forceinline__ bool gemm_fused_trsm(const GemmProblem& p) {
+  return (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_RECT_TRAIL) && p.trsm_next;
 }
 // Queue position of the fused TRSM tasks in a trailing-update launch: after
 // every block of tile column J+1 (their inputs) and early enough that the
@@ -163,7 +168,9 @@ __host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p
 // instead of the large TRSM tasks.
 __host__ __device__ __forceinline__ int64_t gemm_trsm_pos(const GemmProblem& p) {
   const int64_t nupd = gemm_num_items(p);
-  const int64_t col = (int64_t)(p.T - p.J - 1) * (p.b / BM) * (p.b / BN);
+  // blocks of the tiles the solve reads: tile column J+1 (Cholesky) or row
+  // block J+1 of the transposed right-hand side (kriging solve)
+  const int64_t col = (int64_t)(p.mode == GEMM_RECT_TRAIL ? p.Tm : p.T - p.J - 1) * (p.b / BM) * (p.b / BN);
   const int64_t pos = nupd - p.trsm_tail;
   return pos > col ? pos : (col < nupd ? col : nupd);
 }
@@ -173,7 +180,7 @@ __host__ __device__ __forceinline__ bool gemm_task_kind(const GemmProblem& p, in
     idx = task;
     return true;
   }
-  if (p.mode != GEMM_CHOL_TRAIL || !p.trsm_next) {
+  if (!gemm_fused_trsm(p)) {
     idx = task;
     return false;
   }
@@ -241,7 +248,10 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
       pass = (int)(idx % nbn);
       idx /= nbn;
     }
-    trsm_block(it, p, idx, pass, p.mode == GEMM_TRSM_PANEL ? p.panel0 : tri_index(p.J + 2, p.J + 1, p.T));
+    const int64_t panel0 = p.mode == GEMM_TRSM_PANEL   ? p.panel0
+                           : p.mode == GEMM_RECT_TRAIL ? (int64_t)(p.J + 1) * p.Tm
+                                                       : tri_index(p.J + 2, p.J + 1, p.T);
+    trsm_block(it, p, idx, pass, panel0);
     return it;
   }
   const int64_t t = idx / nblk;
@@ -267,6 +277,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
       it.cTile = I * p.Tm + a;
       it.aTile0 = p.J * p.Tm + a;
       it.bTile0 = tri_index(I, p.J, p.T);
+      if (I == p.J + 1 && p.col_gate) it.gate = a;  // row block J+1: the fused solve waits on it
       break;
     }
     case GEMM_SYRK_RECT: {
@@ -391,15 +402,18 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
     const int64_t task = atomicAdd(reinterpret_cast<unsigned long long*>(p.queue), 1ull);
     if (task >= ntasks) break;
     int64_t idx;
-    if (p.mode == GEMM_CHOL_TRAIL && gemm_task_kind(p, task, idx)) {
-      // fused TRSM of panel J+1: the tile's column-(J+1) update blocks have
-      // retired and the side stream published Linv(J+1)
+    if (gemm_fused_trsm(p) && gemm_task_kind(p, task, idx)) {
+      // fused TRSM of panel J+1: the tile's update blocks have retired and
+      // (Cholesky) the look-ahead CTA published Linv(J+1); the kriging solve's
+      // inverses are computed up front (no flag)
       const int tile = (int)(idx / (p.b / BM));
       if (stagger) {  // group 0: release group 1 before blocking (see consumer_loop)
         mbar_arrive(stagger);
         stagger = nullptr;
       }
-      if (!wait_count(p.col_gate + 1 + tile, p.tile_need, info) || !wait_count(p.linv_flag, p.linv_need, info))
+      const int g0 = p.mode == GEMM_CHOL_TRAIL ? 1 : 0;  // Cholesky gate 0 is the diagonal tile
+      if (!wait_count(p.col_gate + g0 + tile, p.tile_need, info) ||
+          (p.linv_flag && !wait_count(p.linv_flag, p.linv_need, info)))
         break;
       fence_proxy_async_global();
     }
