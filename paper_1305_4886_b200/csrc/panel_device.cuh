@@ -319,12 +319,17 @@ static __device__ __noinline__ void tri_inv_diag_device(const double* __restrict
   const int warp = tid >> 5, lane = tid & 31;
   const int nw = TINV_THREADS / 32;
   const int q = lane >> 2, s4 = lane & 3;
-  // block diagonal = Dinv, strictly upper blocks = 0 (below is written per diagonal)
-  for (int idx = tid; idx < b * b; idx += TINV_THREADS) {
-    const int c = idx / b, r = idx % b;
-    const int bi = r / NB, bj = c / NB;
-    if (bi < bj) Linv[idx] = 0.0;
-    else if (bi == bj) Linv[idx] = __ldcg(dinv + (int64_t)bj * NB * NB + (c % NB) * NB + (r % NB));
+  // block diagonal = Dinv, strictly upper blocks = 0 (the blocks below are
+  // written per diagonal): one warp per column, lanes on consecutive rows
+  // (coalesced 16-byte stores, no per-element index arithmetic)
+  for (int c = warp; c < b; c += nw) {
+    const int bj = c / NB;
+    double2* col = reinterpret_cast<double2*>(Linv + (int64_t)c * b);
+    for (int r2 = lane; r2 < bj * NB / 2; r2 += 32) col[r2] = make_double2(0.0, 0.0);
+    if (lane < NB / 2) {
+      const double2* dsrc = reinterpret_cast<const double2*>(dinv + (int64_t)bj * NB * NB + (c % NB) * NB);
+      col[bj * NB / 2 + lane] = __ldcg(dsrc + lane);
+    }
   }
   __threadfence_block();
   named_bar_sync(bar, TINV_THREADS);
