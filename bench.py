@@ -353,7 +353,8 @@ def run_b200(args, world, rank):
                                    "(build + Cholesky + forward solve + logdet + ssq)",
                        "n": n, "tile": args.tile, "theta": THETA.tolist(),
                        "parallelism": (f"2-D block-cyclic tiles over {world} GPUs "
-                                       f"(grid {cl.grid.shape[0]}x{cl.grid.shape[1]}), NCCL panel broadcasts")
+                                       f"(grid {cl.grid.shape[0]}x{cl.grid.shape[1]}), panel exchange: "
+                                       f"{(comm or {}).get('panel_exchange', 'n/a')}")
                                       if world > 1 else "single GPU",
                        "l2": "no flush needed: each step rebuilds and streams the 18.1 GB "
                              "covariance (>> 126 MB L2)"},
