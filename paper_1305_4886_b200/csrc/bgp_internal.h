@@ -41,6 +41,8 @@ struct Ctx {
   size_t gate_cap = 0;
   double* d_linv = nullptr;  // inverse of the current diagonal tile (panel TRSM on DMMA)
   size_t linv_cap = 0;
+  int* d_pass = nullptr;  // per-step pass counters of the parallel fused TRSM
+  size_t pass_cap = 0;
   double* d_linv_all = nullptr;  // inverses of every diagonal tile (kriging solve)
   size_t linv_all_cap = 0;
   int* d_queue = nullptr;  // task counter of standalone GEMM launches
@@ -159,6 +161,12 @@ struct GemmProblem {
   // buffer, so the column passes of a slab read only A and are independent
   // tasks (in place they must run right to left in one task)
   int trsm_oop;
+  // GEMM_CHOL_TRAIL fused TRSM with independent column passes: one task per
+  // (slab, pass), right to left; pass p of a slab stores only after passes
+  // 0 .. p-1 (the columns to its right, which read its block) finished
+  // reading: pass_done[slab * (b / 64) + q] counts the warps of pass q done
+  int trsm_par;
+  int* pass_done;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

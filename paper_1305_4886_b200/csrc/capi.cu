@@ -171,6 +171,7 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_gate) cudaFree(ctx->d_gate);
   if (ctx->d_linv) cudaFree(ctx->d_linv);
   if (ctx->d_linv_all) cudaFree(ctx->d_linv_all);
+  if (ctx->d_pass) cudaFree(ctx->d_pass);
   for (int l = 0; l < 2; ++l)
     if (ctx->d_tail[l]) cudaFree(ctx->d_tail[l]);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
@@ -245,6 +246,18 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
     if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
   }
+  // parallel fused TRSM: per step, one counter per (slab, column pass) of the
+  // next panel (BGP_TRSM_PAR=0: passes of a slab in one task, right to left)
+  static const bool trsm_par = [] {
+    const char* e = getenv("BGP_TRSM_PAR");
+    return !(e && atoi(e) == 0);
+  }();
+  const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);  // any block shape with BM, BN >= 64
+  if (trsm_par) {
+    if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
+    cudaError_t e = cudaMemsetAsync(ctx->d_pass, 0, (size_t)T * pass_stride * sizeof(int), s);
+    if (e != cudaSuccess) return set_err(ctx, "trsm pass counters", e);
+  }
   const int64_t ntiles = tri_count(T);
   const int64_t tsz = (int64_t)b * b;
   int tile_need, diag_need, groups_per_cta;  // gate counts of the chosen GEMM configuration
@@ -315,6 +328,15 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
         p.dinv = ctx->d_dinv;
         p.linv = ctx->d_linv;
         p.diag_need = diag_need;
+        // only where the step is bound by the look-ahead chain (its update
+        // work shorter than POTRF + inverse + solve): there the groups
+        // waiting on passes to their right are idle anyway, while in large
+        // steps the waits would cost update throughput
+        const int k_par = b <= 128 ? 48 : (b <= 256 ? 26 : (b <= 384 ? 22 : 18));
+        if (trsm_par && T - J - 1 <= k_par) {
+          p.trsm_par = 1;
+          p.pass_done = ctx->d_pass + (int64_t)J * pass_stride;
+        }
       }
       if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
       sm.gemm_end = sm.t_end = mk.mark(s);

@@ -101,10 +101,10 @@ constexpr bool EPI_IN_STAGE = false;
 constexpr bool EPI_IN_STAGE = STAGE_BYTES >= GROUP_WARPS * (EPI_ROUNDS - 1) * WSTAGE_BYTES && EPI_ROUNDS > 1;
 #endif
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
-constexpr int BAR_BYTES = 512;
+constexpr int BAR_BYTES = 640;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 32 <= BAR_BYTES, "barrier area");
+static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 48 <= BAR_BYTES, "barrier area");
 
 #ifdef BGP_EXP_STRACE  // probe build: per-stage timestamps (implies the per-item trace)
 #define BGP_EXP_TRACE
@@ -126,6 +126,7 @@ struct Item {
   int store;                 // 1: TMA store of acc (beta = 0 / TRSM), 0: reduce-add of -acc
   int bLinv;                 // 1: B operand from the Linv map (fused TRSM block)
   int gate;                  // >= 0: column-gate index this block signals (update of column J+1)
+  int slab, pass;            // trsm_par TRSM pass: slab index, pass (0 = rightmost); else slab = -1
   bool valid;
 };
 
@@ -154,7 +155,8 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
 // columns a later block still reads.
 __host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p) {
   if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM) * (p.trsm_oop ? p.b / BN : 1);
-  if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next) return (int64_t)(p.T - p.J - 2) * (p.b / BM);
+  if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next)
+    return (int64_t)(p.T - p.J - 2) * (p.b / BM) * (p.trsm_par ? p.b / BN : 1);
   if (p.mode == GEMM_RECT_TRAIL && p.trsm_next) return (int64_t)p.Tm * (p.b / BM);
   return 0;
 }
@@ -241,12 +243,18 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 #endif
   it.bLinv = 0;
   it.gate = -1;
+  it.slab = -1;
+  it.pass = 0;
   int64_t idx;
   if (gemm_task_kind(p, task, idx)) {
     // standalone panel, or the fused TRSM of panel J+1 (tiles J+2 .. T-1)
-    if (p.mode == GEMM_TRSM_PANEL && p.trsm_oop) {  // one independent pass per task
-      pass = (int)(idx % nbn);
+    if ((p.mode == GEMM_TRSM_PANEL && p.trsm_oop) || (p.mode == GEMM_CHOL_TRAIL && p.trsm_par)) {
+      pass = (int)(idx % nbn);  // one pass per task, right to left within a slab
       idx /= nbn;
+      if (p.mode == GEMM_CHOL_TRAIL) {
+        it.slab = (int)idx;
+        it.pass = pass;
+      }
     }
     const int64_t panel0 = p.mode == GEMM_TRSM_PANEL   ? p.panel0
                            : p.mode == GEMM_RECT_TRAIL ? (int64_t)(p.J + 1) * p.Tm
@@ -316,7 +324,10 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
-  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop)) ? p.b / BN : 1;
+  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) &&
+          !(p.mode == GEMM_CHOL_TRAIL && p.trsm_par))
+             ? p.b / BN
+             : 1;
 }
 
 // spin (acquire, exponential back-off, bounded) until *flag >= need or the
@@ -355,8 +366,10 @@ struct BlockSlot {
   int cTile, mrow0, nrow0;
   int nk;     // BK stages
   int lower, store, gate;
+  int slab, pass;  // trsm_par: slab index and pass (-1: not a parallel TRSM pass)
+  int pad[2];
 };
-static_assert(sizeof(BlockSlot) == 32, "slot size");
+static_assert(sizeof(BlockSlot) == 48, "slot size");
 
 struct GroupSmem {
   uint8_t* stages;
@@ -373,7 +386,7 @@ __device__ __forceinline__ GroupSmem group_smem(uint8_t* smem, int g) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + g * (2 * STAGES);
   gs.full = bars;
   gs.empty = bars + STAGES;
-  gs.slot = reinterpret_cast<BlockSlot*>(smem + GROUPS * GROUP_BYTES + 256) + g * STAGES;
+  gs.slot = reinterpret_cast<BlockSlot*>(smem + GROUPS * GROUP_BYTES + 256) + g * STAGES;  // 16-byte aligned
   return gs;
 }
 
@@ -406,7 +419,8 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       // fused TRSM of panel J+1: the tile's update blocks have retired and
       // (Cholesky) the look-ahead CTA published Linv(J+1); the kriging solve's
       // inverses are computed up front (no flag)
-      const int tile = (int)(idx / (p.b / BM));
+      const int per_tile = (p.b / BM) * ((p.mode == GEMM_CHOL_TRAIL && p.trsm_par) ? p.b / BN : 1);
+      const int tile = (int)(idx / per_tile);
       if (stagger) {  // group 0: release group 1 before blocking (see consumer_loop)
         mbar_arrive(stagger);
         stagger = nullptr;
@@ -435,6 +449,8 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
           sl.lower = it.lower;
           sl.store = it.store;
           sl.gate = it.gate;
+          sl.slab = it.slab;
+          sl.pass = it.pass;
         }
 #ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
         mbar_arrive(&gs.full[stage]);
@@ -569,7 +585,8 @@ __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ]
 
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p,
-                                              uint64_t* stagger, const PushMaps* pm) {
+                                              uint64_t* stagger, const PushMaps* pm,
+                                              unsigned long long* info) {
   static_assert((MI == 8 || MI == 4) && NJ == 4 && WN / 16 == 2, "load_frag: 64x32 or 32x32 warp tiles");
   const int wm = gwarp % WARPS_M, wn = gwarp / WARPS_M;
   const int q = lane >> 2, s4 = lane & 3;
@@ -687,6 +704,25 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
+    }
+
+    // Parallel TRSM pass: this warp has read its operands; the block it
+    // stores is read by the passes to its right (q < pass), so wait until
+    // they have read theirs.  Those passes were queued earlier and never
+    // wait on this one.
+    if (it.slab >= 0) {
+      int* pd = p.pass_done + (int64_t)it.slab * (p.b / BN);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(pd + it.pass, 1);
+        for (int q = 0; q < it.pass; ++q)
+          if (!wait_count(pd + q, GROUP_WARPS, info)) {
+            if (info) atomicCAS(info, 0ull, BGP_INFO_DATAFLOW_TIMEOUT);
+            break;
+          }
+      }
+      __syncwarp();
     }
 
     // ------------------------------- epilogue -------------------------------
@@ -880,7 +916,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #ifdef BGP_EXP_ONE_GROUP
     if (g != 0) return;
 #endif
-    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm);
+    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm, info);
   }
 }
 
