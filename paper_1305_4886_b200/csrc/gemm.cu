@@ -974,14 +974,9 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
   int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
   if (p.potrf_tile && grid < 2) grid = 2;  // the look-ahead CTA must not be the only one
-  if (p.potrf_tile) {
-    static bool attr = false;
-    if (!attr) {  // the look-ahead CTA's device POTRF / inverse must fit the ring memory
-      if (tile_potrf_inv_smem_bytes(p.b, true) > (size_t)(GROUPS * GROUP_BYTES))
-        return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
-      attr = true;
-    }
-  }
+  // the look-ahead CTA's device POTRF / inverse must fit the ring memory
+  if (p.potrf_tile && tile_potrf_inv_smem_bytes(p.b, true) > (size_t)(GROUPS * GROUP_BYTES))
+    return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
   gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
                                                                   p.check_info ? ctx->d_info : nullptr, pm);
   ctx->launches++;
