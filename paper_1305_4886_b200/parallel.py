@@ -132,8 +132,10 @@ def dist_cholesky(dist, local, ops, comm):
     Step J: every rank first updates its tiles of column J+1 with panel J.
     Then, on the side stream (ops.side()), the owner of (J+1, J+1) factors
     and inverts it, the inverse is broadcast, process column (J+1) mod Pc
-    solves its panel tiles (A <- A Linv^T on the DMMA GEMM) and the panel is
-    broadcast row chunk by row chunk -- while the rest of the trailing update
+    solves its panel tiles (A <- A Linv^T on the DMMA GEMM) and the panel
+    reaches every rank -- stored by that same TRSM kernel into every rank's
+    panel buffer over NVLink (PanelExchange), or, as the fallback, broadcast
+    row chunk by row chunk over NCCL -- while the rest of the trailing update
     (columns >= J+2, panel J) runs on the compute stream on all SMs but a few
     (ops.update(..., reserve=True)), which the collectives and the small
     panel kernels use.  ops.join_side() then orders step J+1 after panel J+1.
