@@ -25,6 +25,7 @@ struct Ctx {
   int num_sms = 148;
   std::string err;
   int64_t launches = 0;
+  int trace_launches = 0;  // probe builds: timeline slot of the next factorization launch
   // device scratch owned by the context
   unsigned long long* d_info = nullptr;  // [0]: potrf / trsv status
   double* d_red = nullptr;               // reduction partials
@@ -167,6 +168,7 @@ struct GemmProblem {
   // reading: pass_done[slab * (b / 64) + q] counts the warps of pass q done
   int trsm_par;
   int* pass_done;
+  int trace_slot;  // probe builds (BGP_EXP_LTRACE): per-launch timeline record
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

@@ -312,6 +312,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     p.beta = 1.0;
     p.check_info = true;
     p.queue = gate + stride - 2;
+    p.trace_slot = ctx->trace_launches++;
     const bool next = K < J_stop;  // panel K is factored here
     if (la_mode == 1) {
       if (next) {

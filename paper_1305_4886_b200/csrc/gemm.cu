@@ -106,6 +106,20 @@ constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 48 <= BAR_BYTES, "barrier area");
 
+#ifdef BGP_EXP_LTRACE  // probe build: per-launch timeline of the look-ahead chain (globaltimer ns)
+// [0] first CTA start [1] diagonal gate passed [2] POTRF + inverse done
+// [3] first TRSM block start [4] last TRSM block end [5] last update block end
+// [6] last consumer exit [7] T
+__device__ unsigned long long g_ltrace[8192][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define LT_MIN(k) atomicMin(&g_ltrace[p.trace_slot & 8191][k], gtime())
+#define LT_MAX(k) atomicMax(&g_ltrace[p.trace_slot & 8191][k], gtime())
+#define LT_SET(k) (g_ltrace[p.trace_slot & 8191][k] = gtime())
+#endif
 #ifdef BGP_EXP_STRACE  // probe build: per-stage timestamps (implies the per-item trace)
 #define BGP_EXP_TRACE
 __device__ unsigned long long g_strace[148][2][64][20];
@@ -641,6 +655,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     const BlockSlot it = gs.slot[stage];
     if (!it.valid) break;
     const int nk = it.nk;
+#ifdef BGP_EXP_LTRACE
+    if (gwarp == 0 && lane == 0 && p.mode == GEMM_CHOL_TRAIL && it.store) LT_MIN(3);
+#endif
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -843,6 +860,12 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       __syncwarp();
     }
 #endif
+#ifdef BGP_EXP_LTRACE
+    if (gwarp == 0 && lane == 0 && p.mode == GEMM_CHOL_TRAIL) {
+      if (it.store) LT_MAX(4);
+      else LT_MAX(5);
+    }
+#endif
 #ifdef BGP_EXP_TRACE
     if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
       g_trace[blockIdx.x][g][t_idx][2] = clock64();
@@ -853,6 +876,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   release_held();
   if (lane == 0 && store_pending) tma_store_wait_all0();
   if (p.npush > 0) __threadfence_system();  // pushed panel visible to the peers
+#ifdef BGP_EXP_LTRACE
+  if (lane == 0 && p.mode == GEMM_CHOL_TRAIL) LT_MAX(6);
+#endif
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -864,6 +890,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ int s_go;
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
   if (info && *(volatile const unsigned long long*)info != 0ull) return;  // factorization failed
+#ifdef BGP_EXP_LTRACE
+  if (threadIdx.x == 0 && p.mode == GEMM_CHOL_TRAIL) {
+    LT_MIN(0);
+    if (blockIdx.x == 0) g_ltrace[p.trace_slot & 8191][7] = p.T;
+  }
+#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wg = warp >> 2;
@@ -901,10 +933,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (ctid < 256) {
         double* psm = reinterpret_cast<double*>(smem);
         if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
+#ifdef BGP_EXP_LTRACE
+        if (ctid == 0) LT_SET(1);
+#endif
         named_bar_sync(2, 256);
-        if (s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
-                                          p.trsm_next ? p.linv : nullptr, psm, ctid, 2) &&
-            p.trsm_next) {
+        const bool la_ok = s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
+                                                        p.trsm_next ? p.linv : nullptr, psm, ctid, 2);
+#ifdef BGP_EXP_LTRACE
+        if (ctid == 0) LT_SET(2);
+#endif
+        if (la_ok && p.trsm_next) {
           __threadfence();
           named_bar_sync(2, 256);
           if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);
@@ -1037,6 +1075,17 @@ int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Aba
 #if defined(BGP_EXP_TRACE) && !defined(BGP_GEMM_SECONDARY)
 extern "C" int bgp_probe_trace(void* host_out) {
   return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_trace, sizeof(bgp::bk16::g_trace));
+}
+#endif
+#if defined(BGP_EXP_LTRACE) && defined(BGP_GEMM_SECONDARY)
+extern "C" int bgp_probe_ltrace(void* host_out, int reset) {
+  if (reset) {
+    static unsigned long long init[8192][8];
+    for (int i = 0; i < 8192; ++i)
+      for (int k = 0; k < 8; ++k) init[i][k] = (k == 0 || k == 3) ? ~0ull : 0ull;
+    return (int)cudaMemcpyToSymbol(bgp::bk32::g_ltrace, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk32::g_ltrace, sizeof(bgp::bk32::g_ltrace));
 }
 #endif
 #if defined(BGP_EXP_STRACE) && !defined(BGP_GEMM_SECONDARY)
