@@ -97,8 +97,9 @@ size_t tile_potrf_inv_smem_bytes(int b, bool inv);
 // tile kernels
 // info value reserved for a look-ahead wait that never completed (a bug, not data)
 constexpr unsigned long long BGP_INFO_DATAFLOW_TIMEOUT = 1ull << 62;
+// with Linv: the tile's inverse too, built during the factorization
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
-                      const int* gate = nullptr, int gate_need = 0);
+                      const int* gate = nullptr, int gate_need = 0, double* Linv = nullptr);
 // one-CTA block-diagonal inverse of a factored tile (panel_device.cuh)
 int launch_tri_inv(Ctx* ctx, const double* Ltile, const double* dinv, int b, double* Linv, cudaStream_t s,
                    int* done = nullptr);

@@ -292,8 +292,8 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   };
 
   *m_first = mk.mark(s);
-  if ((rc = launch_tile_potrf(ctx, tiles, b, row_base, ctx->d_dinv, s))) return rc;
-  if ((rc = inverse(0))) return rc;
+  if ((rc = launch_tile_potrf(ctx, tiles, b, row_base, ctx->d_dinv, s, nullptr, 0, T > 1 ? ctx->d_linv : nullptr)))
+    return rc;
   *m_p0_out = mk.mark(s);
   if ((rc = panel_solve(0))) return rc;
   *m_t0_out = mk.mark(s);
@@ -747,8 +747,7 @@ int bgp_tile_potrf_inv(bgp_ctx_t ctx, double* tile_ptr, int tile, double* linv, 
   if (rc) return rc;
   const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
-  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, 0, ctx->d_dinv, s))) return rc;
-  if ((rc = launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s))) return rc;
+  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, 0, ctx->d_dinv, s, nullptr, 0, linv))) return rc;
   return read_info(ctx, s, info);
 }
 
@@ -762,9 +761,7 @@ int bgp_tile_potrf_async(bgp_ctx_t ctx, double* tile_ptr, int tile, int64_t row0
   const size_t dinv_bytes = (size_t)(tile / 32) * 32 * 32 * sizeof(double);
   int rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
-  if ((rc = launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s))) return rc;
-  if (linv) return launch_tri_inv(ctx, tile_ptr, ctx->d_dinv, tile, linv, s);
-  return BGP_OK;
+  return launch_tile_potrf(ctx, tile_ptr, tile, row0, ctx->d_dinv, s, nullptr, 0, linv);
 }
 
 int bgp_panel_trsm_inv(bgp_ctx_t ctx, const double* linv, double* A, int64_t count, int tile, void* stream) {

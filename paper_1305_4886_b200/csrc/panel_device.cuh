@@ -168,6 +168,33 @@ __device__ __forceinline__ void trail_block32(double* A, int b, int base_rc, con
       }
 }
 
+// acc (32x32 block as 4x4 8x8 DMMA tiles) += A(32x32) B(32x32): A(r, k) at
+// a[k * lda + r], B(k, c) at bm[c * ldb + k] (both column-major, from L2);
+// all 64 fragments of a k range are loaded before the 128 DMMAs.
+template <bool ASMEM>
+__device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double* __restrict__ a, int64_t lda,
+                                            const double* __restrict__ bm, int64_t ldb, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+#pragma unroll
+  for (int kh = 0; kh < 2; ++kh) {  // two halves of k (16 each) to bound registers
+    double av[4][4], bv[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = kh * 16 + 4 * k + s4;
+        av[k][t] = ASMEM ? a[(int64_t)kk * lda + t * 8 + q] : __ldcg(a + (int64_t)kk * lda + t * 8 + q);
+        bv[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * ldb + kk);
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[k][tr], bv[k][tc]);
+  }
+}
+
 // Right-looking blocked factorization of one b x b tile with 32-wide
 // sub-panels and a one-block look-ahead inside the tile: while warps 1..7
 // apply sub-panel k's trailing update, warp 0 updates, factors and inverts
@@ -176,8 +203,84 @@ __device__ __forceinline__ void trail_block32(double* A, int b, int base_rc, con
 // `sm` is potrf_smem_bytes(b) of shared memory.  Returns false on a
 // non-positive pivot (recorded in *info).  Used by tile_potrf_kernel and,
 // for the look-ahead, by one CTA of the trailing-update launch.
+// Linv[r][j] = -Dinv_r * S with S stored in Linv[r][j] (32x32 blocks of the
+// column-major b x b Linv; Dinv_r column-major 32x32 in global memory): all
+// fragments are loaded before the block is overwritten
+__device__ __forceinline__ void linv_apply_block(const double* __restrict__ Dr, double* Lrj, int b, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+  block_mma32<false>(acc, Dr, NB, Lrj, b, lane);
+  __syncwarp();
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc) {
+      const int row = tr * 8 + q, col = tc * 8 + 2 * s4;
+      Lrj[(int64_t)col * b + row] = -acc[tr][tc][0];
+      Lrj[(int64_t)(col + 1) * b + row] = -acc[tr][tc][1];
+    }
+}
+
+// Row block r of the inverse: Linv[r][r] = Dinv_r (a copy), then
+// Linv[r][j] = -Dinv_r S_rj for j < r, S_rj left in Linv[r][j] by
+// linv_row_partial.  Blocks dealt to warps first .. first + nwarps - 1.
+__device__ __forceinline__ void linv_row_apply(const double* __restrict__ dinv, double* Linv, int b, int r,
+                                               int wid, int nwarps, int lane) {
+  const double* Dr = dinv + (int64_t)r * NB * NB;
+  for (int j = wid; j <= r; j += nwarps) {
+    double* Lrj = Linv + (int64_t)(j * NB) * b + r * NB;
+    if (j == r) {
+      for (int c = 0; c < NB; ++c) Lrj[(int64_t)c * b + lane] = __ldcg(Dr + c * NB + lane);
+    } else {
+      linv_apply_block(Dr, Lrj, b, lane);
+    }
+  }
+}
+
+// S_rj = sum_{m=j}^{r-1} L[r][m] Linv[m][j] into Linv[r][j] for block j (rows
+// < r of Linv final, L's rows up to r complete)
+__device__ __forceinline__ void linv_row_partial(const double* __restrict__ L, bool l_smem, double* Linv, int b,
+                                                 int r, int j, int lane) {
+  const int q = lane >> 2, s4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
+  for (int m = j; m < r; ++m) {
+    const double* a = L + (int64_t)(m * NB) * b + r * NB;
+    const double* bm = Linv + (int64_t)(j * NB) * b + m * NB;
+    if (l_smem) block_mma32<true>(acc, a, b, bm, b, lane);
+    else block_mma32<false>(acc, a, b, bm, b, lane);
+  }
+  double* Lrj = Linv + (int64_t)(j * NB) * b + r * NB;
+#pragma unroll
+  for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < 4; ++tc) {
+      const int row = tr * 8 + q, col = tc * 8 + 2 * s4;
+      Lrj[(int64_t)col * b + row] = acc[tr][tc][0];
+      Lrj[(int64_t)(col + 1) * b + row] = acc[tr][tc][1];
+    }
+}
+
+// With Linv (and dinv) given, the inverse L^{-1} is built during the
+// factorization, row block by row block, in the warps' idle time: row r's
+// partial sums S_rj = sum_m L[r][m] Linv[m][j] need only rows < r of Linv
+// and L's rows up to r, so they run in step r-1's trailing phase next to
+// the trailing blocks; Linv[r][j] = -Dinv_r S_rj follows in step r's
+// sub-panel phase (Dinv_r is produced in step r-1's trailing phase).  (A
+// right-looking order -- every step adding its term to all later rows --
+// spreads the work more evenly but its read-modify-write of the partial
+// sums measured slower.)
+// l_smem: A is a shared-memory copy (see tile_potrf_inv_device).
 static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
-                                  unsigned long long* __restrict__ info, double* sm, int tid, int bar) {
+                                  unsigned long long* __restrict__ info, double* sm, int tid, int bar,
+                                  double* __restrict__ Linv = nullptr, bool l_smem = false) {
   double* D = sm;                // 32 x 33
   double* Dinv_s = D + NB * 33;  // 32 x 33
   double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
@@ -186,8 +289,14 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
   int* s_fail = reinterpret_cast<int*>(col + NB);
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) *s_fail = 0;
-  named_bar_sync(bar, POTRF_THREADS);
   const int nbk = b / NB;
+  if (Linv) {  // strictly upper blocks of the inverse are zero: warp per column
+    for (int c = warp; c < b; c += POTRF_THREADS / 32) {
+      double2* colp = reinterpret_cast<double2*>(Linv + (int64_t)c * b);
+      for (int r2 = lane; r2 < (c / NB) * NB / 2; r2 += 32) colp[r2] = make_double2(0.0, 0.0);
+    }
+  }
+  named_bar_sync(bar, POTRF_THREADS);
   // prologue: factor + invert diagonal block 0
   if (warp == 0) {
     const unsigned fm = warp_potrf32(A, b, 0, D, rdiag, col, lane);
@@ -207,7 +316,15 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
     const int rest = b - c0 - NB;
     // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy),
     // one 32-row block per warp on DMMA: the lane's 32 A values load at once
-    // (one L2 round trip), Dinv (lower triangular, explicit zeros) from smem
+    // (one L2 round trip), Dinv (lower triangular, explicit zeros) from smem;
+    // the inverse's row block kb is finished by the warps after the last
+    // sub-panel block
+    if (Linv) {
+      const int nA = rest / NB;
+      const int w0 = nA % (POTRF_THREADS / 32);  // first warp with no second sub-panel block
+      linv_row_apply(dinv, Linv, b, kb, (warp - w0 + POTRF_THREADS / 32) % (POTRF_THREADS / 32),
+                     POTRF_THREADS / 32, lane);
+    }
     for (int t = warp; t < rest / NB; t += POTRF_THREADS / 32) {
       const int q = lane >> 2, s4 = lane & 3;
       const int r0 = t * NB;  // rows c0 + 32 + r0 .. of the tile
@@ -242,6 +359,7 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
             P[r * PLD + j] = acc[tr][tc][e];
           }
     }
+    if (Linv) __threadfence_block();  // inverse row kb before step kb's partial sums read it
     named_bar_sync(bar, POTRF_THREADS);
     // (B) trailing update in 32x32 blocks; block (0, 0) is diagonal block k+1
     const int nb32 = rest / 32;
@@ -261,47 +379,34 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
         warp_trinv32(D, rdiag, Dinv_s, dinv ? dinv + (int64_t)(kb + 1) * NB * NB : nullptr, lane);
       }
     } else {
-      for (int t = warp; t < nblk; t += POTRF_THREADS / 32 - 1) {  // blocks 1.., row-major lower
+      // the inverse's partial sums of row block kb+1 (kb+1 blocks), then the
+      // trailing blocks 1.. (row-major lower), dealt round-robin to warps 1..7
+      const int nS = Linv ? kb + 1 : 0;
+      for (int u = warp - 1; u < nS + nblk - 1; u += POTRF_THREADS / 32 - 1) {
+        if (u < nS) {
+          linv_row_partial(A, l_smem, Linv, b, kb + 1, u, lane);
+          continue;
+        }
+        const int t = u - nS + 1;
         int bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
         while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
         while (bi * (bi + 1) / 2 > t) --bi;
         trail_block32(A, b, base_rc, P, bi, t - bi * (bi + 1) / 2, lane);
       }
     }
+    __threadfence_block();
     named_bar_sync(bar, POTRF_THREADS);
     if (*s_fail) return false;
+  }
+  if (Linv) {  // the last row block of the inverse
+    linv_row_apply(dinv, Linv, b, nbk - 1, warp, POTRF_THREADS / 32, lane);
+    __threadfence_block();
+    named_bar_sync(bar, POTRF_THREADS);
   }
   return true;
 }
 
 constexpr int TINV_THREADS = 256;
-
-// acc (32x32 block as 4x4 8x8 DMMA tiles) += A(32x32) B(32x32): A(r, k) at
-// a[k * lda + r], B(k, c) at bm[c * ldb + k] (both column-major, from L2);
-// all 64 fragments of a k range are loaded before the 128 DMMAs.
-template <bool ASMEM>
-__device__ __forceinline__ void block_mma32(double (&acc)[4][4][2], const double* __restrict__ a, int64_t lda,
-                                            const double* __restrict__ bm, int64_t ldb, int lane) {
-  const int q = lane >> 2, s4 = lane & 3;
-#pragma unroll
-  for (int kh = 0; kh < 2; ++kh) {  // two halves of k (16 each) to bound registers
-    double av[4][4], bv[4][4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int kk = kh * 16 + 4 * k + s4;
-        av[k][t] = ASMEM ? a[(int64_t)kk * lda + t * 8 + q] : __ldcg(a + (int64_t)kk * lda + t * 8 + q);
-        bv[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * ldb + kk);
-      }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int tr = 0; tr < 4; ++tr)
-#pragma unroll
-        for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[k][tr], bv[k][tc]);
-  }
-}
 
 // Single-CTA inverse of a factored diagonal tile for the look-ahead stream
 // (where only one SM is free): Linv = L^{-1} by block diagonals.  Diagonal
@@ -399,15 +504,7 @@ static __device__ __noinline__ bool tile_potrf_inv_device(double* __restrict__ A
                                                           unsigned long long* __restrict__ info,
                                                           double* __restrict__ Linv, double* sm, int tid, int bar) {
   static_assert(POTRF_THREADS == TINV_THREADS, "one thread set");
-  if (b > SMEM_TILE) {
-    const bool ok = tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar);
-    if (ok && Linv) {
-      __threadfence_block();
-      named_bar_sync(bar, POTRF_THREADS);
-      tri_inv_diag_device<false>(A, dinv, b, Linv, sm, tid, bar);
-    }
-    return ok;
-  }
+  if (b > SMEM_TILE) return tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar, Linv, false);
   double* T = sm;
   double* scratch = sm + (size_t)b * b;
   const int n2 = b * b / 2;
@@ -415,12 +512,7 @@ static __device__ __noinline__ bool tile_potrf_inv_device(double* __restrict__ A
   double2* dst = reinterpret_cast<double2*>(T);
   for (int i = tid; i < n2; i += POTRF_THREADS) dst[i] = __ldcg(src + i);
   named_bar_sync(bar, POTRF_THREADS);
-  const bool ok = tile_potrf_device(T, b, row0, dinv, info, scratch, tid, bar);
-  if (ok && Linv) {
-    __threadfence_block();
-    named_bar_sync(bar, POTRF_THREADS);
-    tri_inv_diag_device<true>(T, dinv, b, Linv, scratch, tid, bar);
-  }
+  const bool ok = tile_potrf_device(T, b, row0, dinv, info, scratch, tid, bar, Linv, true);
   named_bar_sync(bar, POTRF_THREADS);
   double2* out = reinterpret_cast<double2*>(A);
   const double2* Ts = reinterpret_cast<const double2*>(T);

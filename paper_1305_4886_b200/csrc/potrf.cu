@@ -20,15 +20,14 @@ namespace bgp {
 
 size_t potrf_smem_bytes(int b) { return (size_t)(2 * NB * 33 + (b - NB) * PLD + 2 * NB + 2) * sizeof(double); }
 size_t tri_inv_smem_bytes() { return (size_t)(TINV_THREADS / 32) * NB * 33 * sizeof(double); }
-size_t tile_potrf_inv_smem_bytes(int b, bool inv) {
-  size_t scratch = potrf_smem_bytes(b);
-  if (inv && tri_inv_smem_bytes() > scratch) scratch = tri_inv_smem_bytes();
-  return (b <= SMEM_TILE ? (size_t)b * b * sizeof(double) : 0) + scratch;
+size_t tile_potrf_inv_smem_bytes(int b, bool /*inv: the inverse is fused and needs no extra space*/) {
+  return (b <= SMEM_TILE ? (size_t)b * b * sizeof(double) : 0) + potrf_smem_bytes(b);
 }
 
 __global__ void __launch_bounds__(POTRF_THREADS, 1)
     tile_potrf_kernel(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
-                      unsigned long long* __restrict__ info, const int* __restrict__ gate, int gate_need) {
+                      unsigned long long* __restrict__ info, const int* __restrict__ gate, int gate_need,
+                      double* __restrict__ Linv) {
   extern __shared__ double sm[];
   __shared__ int s_skip;
   const int tid = threadIdx.x;
@@ -57,7 +56,7 @@ __global__ void __launch_bounds__(POTRF_THREADS, 1)
   }
   __syncthreads();
   if (s_skip) return;
-  tile_potrf_inv_device(A, b, row0, dinv, info, nullptr, sm, tid, 0);
+  tile_potrf_inv_device(A, b, row0, dinv, info, Linv, sm, tid, 0);
 }
 
 
@@ -221,10 +220,10 @@ void potrf_prepare() {
 }
 
 int launch_tile_potrf(Ctx* ctx, double* tile, int b, int64_t row0, double* dinv, cudaStream_t s,
-                      const int* gate, int gate_need) {
-  const size_t smem = tile_potrf_inv_smem_bytes(b, false);
+                      const int* gate, int gate_need, double* Linv) {
+  const size_t smem = tile_potrf_inv_smem_bytes(b, Linv != nullptr);
   potrf_prepare();
-  tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info, gate, gate_need);
+  tile_potrf_kernel<<<1, POTRF_THREADS, smem, s>>>(tile, b, row0, dinv, ctx->d_info, gate, gate_need, Linv);
   ctx->launches++;
   return check_launch(ctx, "tile_potrf");
 }
