@@ -116,3 +116,17 @@ def test_tail_failure_row(cluster_factory):
     with pytest.raises(NotPositiveDefinite) as info:
         distla.distributed_cholesky(cl, C, "L")
     assert info.value.block_index == bad // lay.block_size + 1
+
+
+def test_large_steps_keep_serial_passes(cluster_factory):
+    """Steps with more trailing tiles than the chain-bound threshold (48 at
+    tile 128) run a slab's TRSM passes as one task; smaller ones as parallel
+    tasks.  n = 56 tiles of 128 covers both regimes in one factorization."""
+    from paper_1305_4886_b200 import distla
+    n = 128 * 56 - 5
+    cl = cluster_factory(tile=128)
+    A = _cov(n, seed=11)
+    C = distla.distribute(cl, "C", A, "triangular", distla.make_layout(n, cl.grid, h=4))
+    L, _ = distla.distributed_cholesky(cl, C, "L")
+    got = distla.collect(cl, L)
+    assert relerr(got, np.linalg.cholesky(A)) <= 1e-12
