@@ -108,12 +108,14 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
  * in place on packed tiles.  info = 0 on success, else the 1-based global
  * row of the first non-positive pivot (LAPACK potrf convention); the caller
  * maps it to NotPositiveDefinite(block) with its layout (kernels.py:146-148).
- * The schedule has a one-panel look-ahead: the next panel's tile POTRF and
- * inverse run on a context-owned side stream (one SM) under the trailing
- * update, which also solves the next panel; the side
- * stream is joined into `stream` before the status read.  BGP_LOOKAHEAD=0
- * in the environment (automatic under CUDA_LAUNCH_BLOCKING=1 or Nsight
- * Compute) runs the same kernels one after another on `stream`. */
+ * The schedule has a one-panel look-ahead inside one launch per step: the
+ * launch's last CTA factors the next panel's diagonal tile (building its
+ * inverse during the factorization) once that tile's update blocks have
+ * retired, and the next panel's solve runs as gated tasks of the same
+ * launch.  Every wait is inside the launch, so the
+ * schedule also holds when kernels are serialised (Nsight Compute).
+ * BGP_LOOKAHEAD=0 in the environment runs POTRF, inverse, solve and update
+ * as separate launches one after another on `stream` (diagnostics). */
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile,
               int64_t* info, void* stream);
 /* With 512 tiles and more than 2*tiles tile rows, bgp_potrf finishes the last
