@@ -242,54 +242,20 @@ __device__ __forceinline__ void linv_row_apply(const double* __restrict__ dinv, 
 }
 
 // S_rj = sum_{m=j}^{r-1} L[r][m] Linv[m][j] into Linv[r][j] for block j (rows
-// < r of Linv final, L's rows up to r complete).  The (r - j) 32x32x32
-// products run as one chain of k-quarters (8 k each): the fragments of
-// quarter c+1 load while quarter c's 32 DMMAs issue (two register sets), so
-// the L2 latency overlaps the math instead of preceding every product.
-template <bool LSMEM>
-__device__ __forceinline__ void linv_quarter_load(const double* __restrict__ L, const double* __restrict__ Linv,
-                                                  int b, int r, int j, int c, double (&fa)[2][4], double (&fb)[2][4],
-                                                  int q, int s4) {
-  const int m = j + (c >> 2), kq = c & 3;
-  const double* a = L + (int64_t)(m * NB) * b + r * NB;
-  const double* bm = Linv + (int64_t)(j * NB) * b + m * NB;
-#pragma unroll
-  for (int k = 0; k < 2; ++k)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int kk = kq * 8 + 4 * k + s4;
-      fa[k][t] = LSMEM ? a[(int64_t)kk * b + t * 8 + q] : __ldcg(a + (int64_t)kk * b + t * 8 + q);
-      fb[k][t] = __ldcg(bm + (int64_t)(t * 8 + q) * b + kk);
-    }
-}
-
-__device__ __forceinline__ void linv_quarter_mma(double (&acc)[4][4][2], const double (&fa)[2][4],
-                                                 const double (&fb)[2][4]) {
-#pragma unroll
-  for (int k = 0; k < 2; ++k)
-#pragma unroll
-    for (int tr = 0; tr < 4; ++tr)
-#pragma unroll
-      for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], fa[k][tr], fb[k][tc]);
-}
-
-template <bool LSMEM>
-__device__ __forceinline__ void linv_row_partial_t(const double* __restrict__ L, double* Linv, int b, int r, int j,
-                                                   int lane) {
+// < r of Linv final, L's rows up to r complete)
+__device__ __forceinline__ void linv_row_partial(const double* __restrict__ L, bool l_smem, double* Linv, int b,
+                                                 int r, int j, int lane) {
   const int q = lane >> 2, s4 = lane & 3;
   double acc[4][4][2];
 #pragma unroll
   for (int tr = 0; tr < 4; ++tr)
 #pragma unroll
     for (int tc = 0; tc < 4; ++tc) acc[tr][tc][0] = acc[tr][tc][1] = 0.0;
-  const int nc = (r - j) * 4;  // k-quarters of the chain
-  double fa0[2][4], fb0[2][4], fa1[2][4], fb1[2][4];
-  linv_quarter_load<LSMEM>(L, Linv, b, r, j, 0, fa0, fb0, q, s4);
-  for (int c = 0; c < nc; c += 2) {
-    linv_quarter_load<LSMEM>(L, Linv, b, r, j, c + 1, fa1, fb1, q, s4);  // nc is a multiple of 4
-    linv_quarter_mma(acc, fa0, fb0);
-    if (c + 2 < nc) linv_quarter_load<LSMEM>(L, Linv, b, r, j, c + 2, fa0, fb0, q, s4);
-    linv_quarter_mma(acc, fa1, fb1);
+  for (int m = j; m < r; ++m) {
+    const double* a = L + (int64_t)(m * NB) * b + r * NB;
+    const double* bm = Linv + (int64_t)(j * NB) * b + m * NB;
+    if (l_smem) block_mma32<true>(acc, a, b, bm, b, lane);
+    else block_mma32<false>(acc, a, b, bm, b, lane);
   }
   double* Lrj = Linv + (int64_t)(j * NB) * b + r * NB;
 #pragma unroll
@@ -300,12 +266,6 @@ __device__ __forceinline__ void linv_row_partial_t(const double* __restrict__ L,
       Lrj[(int64_t)col * b + row] = acc[tr][tc][0];
       Lrj[(int64_t)(col + 1) * b + row] = acc[tr][tc][1];
     }
-}
-
-__device__ __forceinline__ void linv_row_partial(const double* __restrict__ L, bool l_smem, double* Linv, int b,
-                                                 int r, int j, int lane) {
-  if (l_smem) linv_row_partial_t<true>(L, Linv, b, r, j, lane);
-  else linv_row_partial_t<false>(L, Linv, b, r, j, lane);
 }
 
 // With Linv (and dinv) given, the inverse L^{-1} is built during the
