@@ -380,6 +380,112 @@ def run_b200(args, world, rank):
     cl.shutdown()
 
 
+C5_LOGDET_1GPU = -287708.10703490116  # profiles/r01l_configs_tile{256,512}.jsonl (same at both tiles)
+
+
+def run_b200_c5(args, world, rank):
+    """--workload c5 (opt-in): BASELINE config 5, one squared-exponential +
+    nugget factorization of n = 131,072 per step (68.7 GB packed), spread
+    over the job's GPUs; value = aggregate Cholesky TFLOP/s (strong scaling),
+    with the exposed exchange time at N > 1.  The CPU reference cannot hold
+    this matrix (68.7 GB > host RAM), so parity is the log-determinant
+    against this library's own 1-GPU result."""
+    import torch
+
+    from paper_1305_4886_b200 import distla, spawn
+    from paper_1305_4886_b200.gp import CovarianceSpec
+
+    n = 131072
+    X = np.random.default_rng(0).uniform(0, 1, (n, 2))  # SURVEY.md 8d C5 recipe
+    theta = np.array([1.0, 0.02, 0.1])
+    local = 0 if args.debug_share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
+    cl = spawn(world, tile=args.tile, device=local)
+    dev = cl.device
+    spec = CovarianceSpec(cov_fn="gen.sqexp-nugget.cov", cross_cov_fn="gen.sqexp-nugget.cross",
+                          pred_cov_fn="gen.sqexp-nugget.pred", inputs={"coords": X}, n_params=3)
+    lay = distla.make_layout(n, cl.grid)
+    cl.push("c5.inputs", {"coords": X})
+
+    def step():
+        distla.construct_distributed(cl, "c5.C", "triangular", spec.cov_fn, theta,
+                                     inputs_name="c5.inputs", row_layout=lay)
+        L, _ = distla.distributed_cholesky(cl, distla.DistTriangular("c5.C", lay), "c5.L")
+        return L
+
+    for _ in range(args.warmup):
+        step()
+        cl.remote_rm("c5.L")
+    clocks = ClockSampler(dev.index)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = cl.launches()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    e0.record(stream)
+    for k in range(args.steps):
+        L = step()
+        if k + 1 < args.steps:
+            cl.remote_rm("c5.L")
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clk = clocks.stop()
+    ms_max = max_over_ranks(e0.elapsed_time(e1), world)
+    launches = cl.launches() - launches0
+    ld = distla.log_det_from_chol(cl, L)
+    cl.remote_rm("c5.L")
+    tflops = args.steps * n ** 3 / 3 / (ms_max / 1e3) / 1e12
+    comm = None
+    if world > 1:
+        cl.comm_timeline = True
+        step()
+        cl.comm_timeline = False
+        c = cl.last_comm or {}
+        comm = {"comm_ms": max_over_ranks(c.get("comm_ms", 0.0), world),
+                "exposed_comm_ms": max_over_ranks(c.get("exposed_comm_ms", 0.0), world)}
+        cl.remote_rm("c5.L")
+    # end to end: host coords pushed, covariance built, factored, logdet read back
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    cl.push("c5.inputs", {"coords": X})
+    Le = step()
+    distla.log_det_from_chol(cl, Le)
+    torch.cuda.synchronize(dev)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    cl.remote_rm("c5.L")
+    if rank == 0:
+        line = {
+            "metric": "C5 Cholesky FP64 TFLOP/s at n=131,072 (sqexp + nugget)", "value": tflops,
+            "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config 5 recipe, seed 0)",
+            "config": {"workload": "C5: n=131,072 squared-exponential (length 0.02) + nugget 0.1, "
+                                   "covariance build + Cholesky per step",
+                       "n": n, "tile": args.tile,
+                       "parallelism": (f"2-D block-cyclic tiles over {world} GPUs "
+                                       f"(grid {cl.grid.shape[0]}x{cl.grid.shape[1]})")
+                                      if world > 1 else "single GPU",
+                       "l2": "no flush needed: 68.7 GB matrix per step"},
+            "roofline": {"bound": "tensor", "kernel": "whole factorization (n^3/3 per step)",
+                         "achieved": tflops, "peak": FP64_DMMA_PEAK * world, "unit": "TFLOP/s",
+                         "frac": tflops / (FP64_DMMA_PEAK * world), "traffic": None},
+            "parity": {"logdet": ld, "ref_logdet_1gpu": C5_LOGDET_1GPU,
+                       "rel_err": abs(ld - C5_LOGDET_1GPU) / abs(C5_LOGDET_1GPU), "tol": 1e-10,
+                       "note": "the CPU reference cannot hold C5; reference = this library on 1 GPU"},
+            "clocks": clk, "gpu_launches": launches,
+            "e2e": {"value": n ** 3 / 3 / e2e_s / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": 8 * world},
+            "cpu_baseline": None,
+        }
+        if comm is not None:
+            line["communication"] = comm
+        print(json.dumps(line), flush=True)
+    cl.shutdown()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -390,6 +496,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-samples", type=int, default=30)  # ~11 s of host work
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: the BASELINE metric (default); c5: config 5 Cholesky scaling")
     ap.add_argument("--debug-share-gpu", action="store_true",
                     help="test only: every rank on cuda:0 over gloo, to exercise the N > 1 path "
                          "on a one-GPU box (the numbers mean nothing)")
@@ -397,6 +505,8 @@ def main():
     world, rank = dist_setup(args.impl, args.debug_share_gpu)
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.workload == "c5":
+        run_b200_c5(args, world, rank)
     else:
         run_b200(args, world, rank)
     if world > 1:
