@@ -3,14 +3,14 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 SRC_DIR := paper_1305_4886_b200/csrc
-SRCS := $(SRC_DIR)/capi.cu $(SRC_DIR)/cov.cu $(SRC_DIR)/potrf.cu $(SRC_DIR)/gemm.cu $(SRC_DIR)/solve.cu $(SRC_DIR)/rng.cu $(SRC_DIR)/trsv.cu $(SRC_DIR)/gemm_bk32.cu
+SRCS := $(SRC_DIR)/capi.cu $(SRC_DIR)/cov.cu $(SRC_DIR)/potrf.cu $(SRC_DIR)/gemm.cu $(SRC_DIR)/solve.cu $(SRC_DIR)/rng.cu $(SRC_DIR)/trsv.cu
 HDRS := $(SRC_DIR)/bgp_common.cuh $(SRC_DIR)/bgp_internal.h $(SRC_DIR)/panel_device.cuh include/bgp.h
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB := paper_1305_4886_b200/libbgp.so
 
 all: $(LIB)
 
-build/%.o: $(SRC_DIR)/%.cu $(HDRS) $(SRC_DIR)/gemm.cu
+build/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 

@@ -18,10 +18,13 @@ step).  `roofline` is the trailing-update DMMA kernel (the dominant one)
 against the measured FP64 DMMA peak; `cpu_baseline` / `--impl reference` time
 the reference algorithm on the host cores (oracle/cpu_baseline.py).
 
-Under torchrun (N > 1) the evaluation is sharded: one process per GPU, the
-covariance tiles spread 2-D block-cyclically (paper_1305_4886_b200/parallel.py),
-panel broadcasts over NCCL; `value` is evaluations/s of the whole job (strong
-scaling: the problem size is fixed).
+With --gpus N > 1 the evaluation is sharded over N GPUs of the box: one
+process per GPU (started here under torch.distributed.run when the caller
+did not launch the ranks itself), the covariance tiles spread 2-D
+block-cyclically (paper_1305_4886_b200/parallel.py), one launch per sweep
+step with the panel solve + NVLink push inside it; `value` is evaluations/s
+of the whole job (strong scaling: the problem size is fixed).  N larger than
+the visible GPU count is refused.
 """
 
 import argparse
@@ -158,20 +161,39 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
+def full_eval_record():
+    """A timed FULL reference-algorithm evaluation at C4 on a GPU box's host
+    (tools/cpu_full_eval.py, committed under profiles/), reported beside the
+    sampler's extrapolation; None if none is committed."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_cpu_full_eval.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        rec = json.load(f)
+    rec["file"] = os.path.relpath(files[-1], ROOT)
+    return rec
+
+
 def cpu_reference(samples, X):
+    """Sampled reference evaluation time: the median over `samples` samples
+    of each one's extrapolated evaluation time."""
     from oracle.cpu_baseline import ReferenceSampler, host_cores
     s = ReferenceSampler(X, THETA)
-    best, walls = None, []
+    evals, chols, walls = [], [], []
     for _ in range(samples):
         t, wall = s.sample()
         walls.append(wall)
-        best = t if best is None else {k: min(best[k], t[k]) for k in t}
-    total, chol = s.extrapolate(best)
+        total, chol = s.extrapolate(t)
+        evals.append(total)
+        chols.append(chol)
+    total, chol = statistics.median(evals), statistics.median(chols)
     n = s.n
     return {"evals_per_s": 1.0 / total, "eval_s": total, "chol_s": chol,
+            "eval_s_range": [min(evals), max(evals)],
             "chol_tflops": n ** 3 / 3 / chol / 1e12, "cores": host_cores(),
-            "sample": s.describe() + f"; best-of-{samples} per-op medians; "
-                      f"{sum(walls):.1f} s of sampling", "walls": walls}
+            "sample": s.describe() + f"; median over {samples} samples of the extrapolated "
+                      f"evaluation; {sum(walls):.1f} s of sampling", "walls": walls}
 
 
 def run_reference(args, world, rank):
@@ -181,35 +203,40 @@ def run_reference(args, world, rank):
         return
     from oracle.cpu_baseline import ReferenceSampler, host_cores
     s = ReferenceSampler(X, THETA)
-    per_step = []
+    per_step, per_step_chol = [], []
     for _ in range(args.warmup):
         s.sample()
-    best = None
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        # one step = REF_SAMPLES samples (~3 s of host work)
-        step_best = None
+        # one step = REF_SAMPLES samples (~3 s of host work): the step's
+        # evaluation time is the median of the samples' extrapolations
+        ev, ch = [], []
         for _ in range(REF_SAMPLES):
             t, _ = s.sample()
-            step_best = t if step_best is None else {k: min(step_best[k], t[k]) for k in t}
-        per_step.append(s.extrapolate(step_best)[0])
-        best = step_best if best is None else {k: min(best[k], step_best[k]) for k in step_best}
+            a, c = s.extrapolate(t)
+            ev.append(a)
+            ch.append(c)
+        per_step.append(statistics.median(ev))
+        per_step_chol.append(statistics.median(ch))
     wall = time.perf_counter() - t0
-    total, chol = s.extrapolate(best)
+    total, chol = statistics.median(per_step), statistics.median(per_step_chol)
     value = 1.0 / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": None,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 4 recipe)",
         "config": {"workload": "C4: n=67,275 exponential GP log-likelihood (reference "
                                "P=1 block sweep, block 990)", "n": 67275},
         "cholesky_tflops": 67275 ** 3 / 3 / chol / 1e12,
         "extrapolated_eval_s": total,
         "per_step_eval_s": per_step,
+        "measured_full_eval": full_eval_record(),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": host_cores(),
                          "kind": "port", "sample": s.describe() +
-                         f"; each step = {REF_SAMPLES} samples, value from best-of per-op medians"},
+                         f"; each step = {REF_SAMPLES} samples, step value = median of their "
+                         "extrapolations, line value = median over steps",
+                         "extrapolated_eval_s": total, "measured_full_eval": full_eval_record()},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -276,9 +303,15 @@ def run_b200(args, world, rank):
     chol_ms = prof[8] / facts  # first to last launch of each factorization (POTRF overlaps)
     if prof[7] == 0:  # sharded path: host-synchronised time of the last factorization
         chol_ms = max_over_ranks(cl.last_cholesky_ms or 0.0, world)
+    # the update launches carry the whole factorization (the look-ahead POTRF,
+    # inverse and panel TRSM run inside them), so the algorithmic work of
+    # their summed event time is the unpadded n^3/3; the
+    # padded-tile flops they execute are reported beside it
+    executed_flops = gemm_flops / facts
+    gemm_flops = n ** 3 / 3 * facts
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     peak = FP64_DMMA_PEAK
-    roof_kernel = "gemm_dmma_kernel (trailing SYRK/GEMM)"
+    roof_kernel = "gemm_dmma_kernel (trailing SYRK/GEMM with the in-launch POTRF/TRSM)"
     if world > 1:  # aggregate: the whole factorization against N x the per-GPU peak
         gemm_tflops = n ** 3 / 3 / (chol_ms / 1e3) / 1e12 if chol_ms else 0.0
         gemm_flops, facts = n ** 3 / 3, 1
@@ -306,9 +339,9 @@ def run_b200(args, world, rank):
                 "panel_exchange": ("fused TRSM + NVLink peer stores (bgp_panel_trsm_push)"
                                    if cl.__dict__.get("_panel_xchg", {}).get("x") is not None
                                    and cl._panel_xchg["x"].ok else "NCCL broadcasts"),
-                "how": "CUDA events around each collective (inverse broadcast, panel broadcasts or "
-                       "push barriers; side stream) and each trailing update (compute stream) of one "
-                       "untimed evaluation; exposed = collective time not covered by any update; "
+                "how": "CUDA events around each step barrier (push exchange) or panel broadcast "
+                       "(fallback) and each step launch of one untimed evaluation (one stream: every "
+                       "barrier wait is exposed, including waiting for the slowest rank); "
                        "max over ranks"}
 
     # end to end through the public API from host buffers (pinned), every step
@@ -340,13 +373,15 @@ def run_b200(args, world, rank):
         r = cpu_reference(args.cpu_samples, X)
         cpu = {"value": r["evals_per_s"], "unit": "evals/s", "cores": r["cores"],
                "kind": "port", "sample": r["sample"],
-               "cholesky_tflops": r["chol_tflops"], "extrapolated_eval_s": r["eval_s"]}
+               "cholesky_tflops": r["chol_tflops"], "extrapolated_eval_s": r["eval_s"],
+               "extrapolated_eval_s_range": r["eval_s_range"],
+               "measured_full_eval": full_eval_record()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else None,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config 4 recipe, frozen inputs)",
             "config": {"workload": "C4: n=67,275 exponential GP log-likelihood "
@@ -366,6 +401,7 @@ def run_b200(args, world, rank):
                          "peak_source": "measured DMMA.8x8x4 loop (profiles/r01_fp64_peaks.jsonl); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "algorithmic_flops_per_eval": gemm_flops / facts,
+                         "executed_flops_per_eval": executed_flops if world == 1 else None,
                          "launches_per_eval": gemm_launches / facts,
                          "cublas_dgemm_tflops": CUBLAS_DGEMM},
             "parity": parity,
@@ -460,7 +496,7 @@ def run_b200_c5(args, world, rank):
             "metric": "C5 Cholesky FP64 TFLOP/s at n=131,072 (sqexp + nugget)", "value": tflops,
             "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if world > 1 else None, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config 5 recipe, seed 0)",
             "config": {"workload": "C5: n=131,072 squared-exponential (length 0.02) + nugget 0.1, "
                                    "covariance build + Cholesky per step",
@@ -486,6 +522,25 @@ def run_b200_c5(args, world, rank):
     cl.shutdown()
 
 
+def launch_ranks(args):
+    """--gpus N without a launcher: start N ranks (one process per GPU) under
+    torch.distributed.run and exit with their status; rank 0 prints the line."""
+    import socket
+
+    import torch
+    ndev = torch.cuda.device_count()
+    if args.gpus > ndev and not args.debug_share_gpu:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {ndev} GPU(s) are visible; "
+                 "refusing to time fewer GPUs than requested")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -502,6 +557,11 @@ def main():
                     help="test only: every rank on cuda:0 over gloo, to exercise the N > 1 path "
                          "on a one-GPU box (the numbers mean nothing)")
     args = ap.parse_args()
+    env_world = int(os.environ.get("WORLD_SIZE", "1"))
+    if env_world > 1 and env_world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+    if env_world == 1 and args.gpus > 1 and args.impl == "b200":
+        launch_ranks(args)  # does not return
     world, rank = dist_setup(args.impl, args.debug_share_gpu)
     if args.impl == "reference":
         run_reference(args, world, rank)

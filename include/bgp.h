@@ -267,11 +267,32 @@ int bgp_panel_trsm_push(bgp_ctx_t ctx, const double* linv, double* A, int64_t co
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase,
                     const double* Bbase, const int32_t* triples /*device, 4 per*/,
                     int64_t count, int tile, void* stream);
-/* bgp_tile_update on at most max_ctas CTAs (leaves SMs to concurrent work
- * such as NCCL collectives on another stream). */
-int bgp_tile_update_limited(bgp_ctx_t ctx, double* Cbase, const double* Abase,
-                            const double* Bbase, const int32_t* triples, int64_t count,
-                            int tile, int max_ctas, void* stream);
+
+/* ---- one rank's share of the distributed block sweep ----------------------
+ * Replaces the per-worker body of _cholesky_sweep (bg/distla/kernels.py:
+ * 139-194) on a 2-D block-cyclic tile distribution; the host (parallel.py)
+ * orders the steps with one stream-ordered barrier each.
+ * bgp_dist_begin: zero the per-step counters of a T-step sweep, reset the
+ *   status.
+ * bgp_dist_step: step J as ONE launch.  items (device, 4 int32 per tuple):
+ *   (C local tile, A panel slot, B panel slot, flags), flags bit 0 = C is a
+ *   diagonal tile (lower part only), bits 8.. = gate + 1; the first
+ *   col_items tuples update tile column J+1 (gate 0 the diagonal tile, 1..
+ *   the rank's panel tiles in local order).  With diag != NULL the launch
+ *   also factors that tile (row diag_row0 for the status) once its update
+ *   retired (kernels.py:144-153 POTRF), inverts it, and solves the rank's
+ *   trsm_count panel tiles local[trsm_first ..] in place (kernels.py:155-165
+ *   TRSM) -- every solved block is also stored into tile slot0 + t of each of
+ *   the ndst (<= 8) panel buffers dst[] (own and peers', IPC-mapped), which
+ *   replaces the "col" sends of kernels.py:167-187.  Launches are skipped
+ *   once the status records a failure. */
+int bgp_dist_begin(bgp_ctx_t ctx, int T, int tile, void* stream);
+int bgp_dist_step(bgp_ctx_t ctx, int J, double* local, int64_t nlocal,
+                  const double* panel, int64_t npanel, const int32_t* items,
+                  int64_t count, int64_t col_items, double* diag, int64_t diag_row0,
+                  int64_t trsm_first, int64_t trsm_count, int trsm_par,
+                  double* const* dst, int ndst, int64_t slot0, int64_t dst_tiles,
+                  int tile, void* stream);
 
 /* ---- measurement ----------------------------------------------------------
  * When profiling is on, bgp_potrf brackets every launch with CUDA events

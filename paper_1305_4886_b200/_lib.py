@@ -11,7 +11,7 @@ import os
 from .errors import BackendUnavailable
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# BGP_LIB_PATH (diagnostics): load an alternative build, e.g. a probe variant
+# BGP_LIB_PATH (diagnostics): load an alternative build of the library
 LIB_PATH = os.environ.get("BGP_LIB_PATH") or os.path.join(_HERE, "libbgp.so")
 
 BGP_OK = 0
@@ -79,7 +79,9 @@ SIGNATURES = {
                                    _int, _i64, _i64, _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
-    "bgp_tile_update_limited": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _int, _c_dp]),
+    "bgp_dist_begin": (_int, [ctypes.c_void_p, _int, _int, _c_dp]),
+    "bgp_dist_step": (_int, [ctypes.c_void_p, _int, _c_dp, _i64, _c_dp, _i64, _c_dp, _i64, _i64, _c_dp, _i64,
+                             _i64, _i64, _int, ctypes.POINTER(ctypes.c_void_p), _int, _i64, _i64, _int, _c_dp]),
     "bgp_construct_tiles": (_int, [ctypes.c_void_p, ctypes.POINTER(Generator), _c_dp, _i64, _int, _int,
                                    _c_dp, _i64, _c_dp, _c_dp]),
     "bgp_tile_trsv": (_int, [ctypes.c_void_p, _c_dp, _int, _i64, _i64, _c_dp, _int,

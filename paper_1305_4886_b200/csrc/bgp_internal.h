@@ -25,7 +25,6 @@ struct Ctx {
   int num_sms = 148;
   std::string err;
   int64_t launches = 0;
-  int trace_launches = 0;  // probe builds: timeline slot of the next factorization launch
   // device scratch owned by the context
   unsigned long long* d_info = nullptr;  // [0]: potrf / trsv status
   double* d_red = nullptr;               // reduction partials
@@ -46,10 +45,15 @@ struct Ctx {
   size_t pass_cap = 0;
   double* d_linv_all = nullptr;  // inverses of every diagonal tile (kriging solve)
   size_t linv_all_cap = 0;
-  int* d_queue = nullptr;  // task counter of standalone GEMM launches
-  size_t queue_cap = 0;
+  // per-launch task counters (+ look-ahead tickets) of GEMM launches that do
+  // not bring their own: a ring of 16-byte slots, one per launch
+  static constexpr int QUEUE_RING = 1024;
+  int* d_queue_ring = nullptr;
+  size_t queue_ring_cap = 0;
+  unsigned queue_next = 0;
   double* d_tail[2] = {nullptr, nullptr};  // re-tiled trailing triangles of the Cholesky tail
   size_t tail_cap[2] = {0, 0};
+  int dist_T = 0, dist_b = 0;  // bgp_dist_begin: tile rows and tile size of the current sweep
   int tail_tiles = 32;  // 512-tile rows finished on 256 tiles (half as many 256 rows on 128; bgp_set_tail)
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)
@@ -126,7 +130,7 @@ struct GemmProblem {
   int J;    // panel index (trailing modes)
   int Tm;   // tile rows of a transposed rectangular object
   int Tn;   // tile columns of a transposed rectangular object
-  int64_t count;  // GEMM_LIST: number of (C, A, B, lower) tuples
+  int64_t count;  // GEMM_LIST: number of (C, A, B, flags) tuples
   const int32_t* items;
   double alpha, beta;  // D = beta*C + alpha*sum(A B^T)
   bool check_info;     // skip the launch when ctx->d_info records a failure
@@ -169,7 +173,15 @@ struct GemmProblem {
   // reading: pass_done[slab * (b / 64) + q] counts the warps of pass q done
   int trsm_par;
   int* pass_done;
-  int trace_slot;  // probe builds (BGP_EXP_LTRACE): per-launch timeline record
+  // GEMM_LIST as one step of the distributed sweep: the first col_items
+  // tuples update tile column J+1 (their flags carry the gates); the fused
+  // TRSM solves the rank's trsm_count panel tiles from local index panel0
+  // (and pushes them when npush > 0)
+  int64_t col_items;
+  int64_t trsm_count;
+  // zeroed int: the first CTA to take a ticket is the look-ahead CTA
+  // (null: launch_gemm provides one)
+  int* role_ticket;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

@@ -172,6 +172,7 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_linv) cudaFree(ctx->d_linv);
   if (ctx->d_linv_all) cudaFree(ctx->d_linv_all);
   if (ctx->d_pass) cudaFree(ctx->d_pass);
+  if (ctx->d_queue_ring) cudaFree(ctx->d_queue_ring);
   for (int l = 0; l < 2; ++l)
     if (ctx->d_tail[l]) cudaFree(ctx->d_tail[l]);
   for (int i = 0; i < ctx->events_cap; ++i) cudaEventDestroy(ctx->events[i]);
@@ -238,7 +239,8 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   const size_t dinv_bytes = (size_t)nbk * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
-  // published, [stride-2, stride) the 64-bit task counter of the step's launch
+  // published, [T+1] look-ahead ticket, [stride-2, stride) the 64-bit task
+  // counter of the step's launch
   const int stride = (T + 4 + 1) & ~1;
   if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
@@ -312,7 +314,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     p.beta = 1.0;
     p.check_info = true;
     p.queue = gate + stride - 2;
-    p.trace_slot = ctx->trace_launches++;
+    p.role_ticket = gate + T + 1;
     const bool next = K < J_stop;  // panel K is factored here
     if (la_mode == 1) {
       if (next) {
@@ -850,21 +852,93 @@ int bgp_panel_trsm(bgp_ctx_t ctx, const double* Ld, double* A, int64_t count, in
   return launch_panel_trsm(ctx, Ld, ctx->d_dinv, A, count, tile, 0, s, false);
 }
 
-int bgp_tile_update_limited(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase,
-                            const int32_t* triples, int64_t count, int tile, int max_ctas, void* stream) {
-  if (!valid_tile(tile) || count < 0) return BGP_E_ARG;
-  if (count == 0) return BGP_OK;
+// ---- distributed sweep (one rank's share of bg/distla/kernels.py:139-194) ----
+// Per-step counter blocks (gates, inverse flag, look-ahead ticket, task
+// counter) and pass counters for T steps, zeroed on the stream; status reset.
+int bgp_dist_begin(bgp_ctx_t ctx, int T, int tile, void* stream) {
+  if (!valid_tile(tile) || T < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int b = tile;
+  int rc;
+  const int stride = (T + 4 + 1) & ~1;
+  const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);
+  if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, (size_t)(b / 32) * 32 * 32 * sizeof(double))))
+    return rc;
+  if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
+  cudaError_t e = cudaMemsetAsync(ctx->d_gate, 0, (size_t)T * stride * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_pass, 0, (size_t)T * pass_stride * sizeof(int), s);
+  if (e != cudaSuccess) return set_err(ctx, "sweep counters", e);
+  ctx->dist_T = T;
+  ctx->dist_b = b;
+  gemm_prepare();
+  potrf_prepare();
+  return reset_info(ctx, s);
+}
+
+// Step J of a rank's sweep as ONE launch: the update of its tiles (and
+// diagonal shadows) by panel J, column J+1 first; with `diag`, the launch's
+// look-ahead CTA factors tile (J+1, J+1) (the rank's own, or its shadow copy)
+// once its update retired, inverts it, and the fused TRSM tasks solve the
+// rank's trsm_count panel tiles of column J+1 in place -- each storing every
+// solved block also into the ndst panel buffers (own + peers', over NVLink).
+int bgp_dist_step(bgp_ctx_t ctx, int J, double* local, int64_t nlocal, const double* panel, int64_t npanel,
+                  const int32_t* items, int64_t count, int64_t col_items, double* diag, int64_t diag_row0,
+                  int64_t trsm_first, int64_t trsm_count, int trsm_par, double* const* dst, int ndst,
+                  int64_t slot0, int64_t dst_tiles, int tile, void* stream) {
+  const int T = ctx->dist_T;
+  if (!valid_tile(tile) || tile != ctx->dist_b || J < 0 || J + 1 >= T || count < 0 || col_items < 0 ||
+      col_items > count || trsm_count < 0 || (trsm_count > 0 && !diag) || (col_items > 0 && !diag) ||
+      trsm_first < 0 || trsm_first + trsm_count > nlocal || ndst < 0 || ndst > BGP_MAX_PUSH ||
+      (ndst > 0 && (!dst || slot0 < 0 || slot0 + trsm_count > dst_tiles)) || nlocal < 1 || npanel < 1)
+    return BGP_E_ARG;
+  if (count == 0 && !diag) return BGP_OK;
+  const int b = tile;
+  const int stride = (T + 4 + 1) & ~1;
+  const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);
+  int* gate = ctx->d_gate + (int64_t)J * stride;
+  int tile_need, diag_need, groups_per_cta;
+  gemm_block_counts(b, &tile_need, &diag_need, &groups_per_cta);
+  double* bases[BGP_MAX_PUSH];
+  for (int d = 0; d < ndst; ++d) bases[d] = dst[d] + slot0 * (int64_t)b * b;
   GemmProblem p{};
   p.mode = GEMM_LIST;
-  p.b = tile;
+  p.b = b;
+  p.J = J;
   p.count = count;
-  p.items = triples;
+  p.items = items;
   p.alpha = -1.0;
   p.beta = 1.0;
-  p.check_info = false;
-  p.grid_limit = max_ctas > 0 ? max_ctas : 0;
-  const int64_t big = (int64_t)1 << 30;
-  return launch_gemm(ctx, p, Cbase, Abase, big, Bbase, big, big, (cudaStream_t)stream);
+  p.check_info = true;
+  p.queue = gate + stride - 2;
+  p.role_ticket = gate + T + 1;
+  p.col_items = col_items;
+  if (diag) {
+    p.col_gate = gate;
+    p.potrf_tile = diag;
+    p.potrf_row0 = diag_row0;
+    p.dinv = ctx->d_dinv;
+    p.linv = ctx->d_linv;
+    p.diag_need = diag_need;
+    p.tile_need = tile_need;
+    p.linv_flag = gate + T;
+    p.linv_need = b / 32;
+    p.trsm_next = trsm_count > 0;
+    p.trsm_count = trsm_count;
+    p.panel0 = trsm_first;
+    p.trsm_tail = 6 * groups_per_cta * ctx->num_sms;
+    if (trsm_par && trsm_count > 0) {
+      p.trsm_par = 1;
+      p.pass_done = ctx->d_pass + (int64_t)J * pass_stride;
+    }
+    if (ndst > 0 && trsm_count > 0) {
+      p.npush = ndst;
+      p.push_dst = bases;
+      p.push_tiles = dst_tiles - slot0;
+    }
+  }
+  return launch_gemm(ctx, p, local, panel, npanel, panel, npanel, nlocal, (cudaStream_t)stream, ctx->d_linv);
 }
 
 int bgp_tile_update(bgp_ctx_t ctx, double* Cbase, const double* Abase, const double* Bbase, const int32_t* triples,

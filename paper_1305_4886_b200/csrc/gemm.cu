@@ -34,15 +34,8 @@
 #include <stdlib.h>
 #include <string.h>
 
-// Compiled twice: here with the BK = 16 configuration (namespace bgp::bk16)
-// and from gemm_bk32.cu with BK = 32 (bgp::bk32); launch_gemm picks bk32
-// unless BGP_GEMM_CFG=16.
-#ifndef BGP_GEMM_NS
-#define BGP_GEMM_NS bk16
-#endif
-
 namespace bgp {
-namespace BGP_GEMM_NS {
+namespace dmma {
 
 // Tile configuration.  One CTA per SM, three warpgroups:
 //   WG0  producers: warp 0 feeds consumer group 0's ring, warp 1 group 1's
@@ -52,30 +45,12 @@ namespace BGP_GEMM_NS {
 // Each group's producer claims blocks from the launch's task queue, and the
 // two groups run concurrently (half a block apart), so one group's epilogue
 // overlaps the other group's main loop and the DMMA pipe never drains.
-// Compiled twice (see below): BK = 32 is the production configuration at
-// every tile size, BK = 16 a diagnostic (BGP_GEMM_CFG=16); the other
-// BGP_GEMM_* / BGP_EXP_* macros select probe builds (tools/gemm_probe.sh).
-#if defined(BGP_GEMM_3G)  // three consumer groups of 2x2 warps of 32x32: 64x64 blocks
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 16;
-constexpr int GROUPS = 3;
-constexpr int WM = 32, WN = 32;                // warp tile
-constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 144;
-#elif defined(BGP_GEMM_BK16S2)  // probe: 2 stages of BK = 16, whole 64-row warp tile staged at once
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 2, EPI_ROWS = 64;
-constexpr int GROUPS = 2;
-constexpr int WM = 64, WN = 32;
-constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
-#elif defined(BGP_GEMM_BK32)  // 2 stages of BK = 32, epilogue in 16-row rounds
+// Two stages of BK = 32 per group at every tile size; the epilogue goes out
+// in 16-row rounds (DESIGN.md section 5 records the alternatives measured).
 constexpr int BM = 128, BN = 64, BK = 32, STAGES = 2, EPI_ROWS = 16;
 constexpr int GROUPS = 2;
 constexpr int WM = 64, WN = 32;
 constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
-#else  // tiles < 512: 3 stages of BK = 16, epilogue in 32-row rounds
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, EPI_ROWS = 32;
-constexpr int GROUPS = 2;
-constexpr int WM = 64, WN = 32;
-constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
-#endif
 constexpr int WARPS_M = 2, WARPS_N = 2;       // per consumer group
 constexpr int GROUP_WARPS = WARPS_M * WARPS_N;
 constexpr int THREADS = 128 * (GROUPS + 1);
@@ -95,39 +70,13 @@ constexpr int CBUF_BYTES = GROUP_WARPS * WSTAGE_BYTES;
 // the epilogue stages them in the block's last stage (released to the
 // producer only once the bulk reads are done, early in the next block) and
 // the last round in the warp's own slice: no wait between rounds.
-#if defined(BGP_EXP_NO_EPI) || defined(BGP_EPI_RED) || defined(BGP_EXP_EPI_SLICE)
-constexpr bool EPI_IN_STAGE = false;
-#else
 constexpr bool EPI_IN_STAGE = STAGE_BYTES >= GROUP_WARPS * (EPI_ROUNDS - 1) * WSTAGE_BYTES && EPI_ROUNDS > 1;
-#endif
 constexpr int GROUP_BYTES = STAGES * STAGE_BYTES + CBUF_BYTES;
 constexpr int BAR_BYTES = 640;
 constexpr int SMEM_BYTES = GROUPS * GROUP_BYTES + BAR_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 48 <= BAR_BYTES, "barrier area");
 
-#ifdef BGP_EXP_LTRACE  // probe build: per-launch timeline of the look-ahead chain (globaltimer ns)
-// [0] first CTA start [1] diagonal gate passed [2] POTRF + inverse done
-// [3] first TRSM block start [4] last TRSM block end [5] last update block end
-// [6] last consumer exit [7] T
-__device__ unsigned long long g_ltrace[8192][8];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define LT_MIN(k) atomicMin(&g_ltrace[p.trace_slot & 8191][k], gtime())
-#define LT_MAX(k) atomicMax(&g_ltrace[p.trace_slot & 8191][k], gtime())
-#define LT_SET(k) (g_ltrace[p.trace_slot & 8191][k] = gtime())
-#endif
-#ifdef BGP_EXP_STRACE  // probe build: per-stage timestamps (implies the per-item trace)
-#define BGP_EXP_TRACE
-__device__ unsigned long long g_strace[148][2][64][20];
-#endif
-#ifdef BGP_EXP_TRACE  // probe build: per-item timestamps of warp 0 of each group
-constexpr int TRACE_ITEMS = 64;
-__device__ unsigned long long g_trace[148][GROUPS][TRACE_ITEMS][6];
-#endif
 
 struct Item {
   int cTile, aTile0, bTile0;  // tile indices (< 2^31: 1.4e5 tiles at n = 131,072, b = 256)
@@ -167,16 +116,22 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
 // trailing update for the next panel): a 128-row slab of a panel tile, its
 // b/64 column blocks right to left, so the in-place solve never overwrites
 // columns a later block still reads.
+// Cholesky-type fused TRSM (the packed-triangle sweep, or a rank's tile list
+// in the distributed sweep) whose column passes are independent tasks
+__host__ __device__ __forceinline__ bool gemm_par_passes(const GemmProblem& p) {
+  return (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST) && p.trsm_par;
+}
 __host__ __device__ __forceinline__ int64_t gemm_trsm_tasks(const GemmProblem& p) {
   if (p.mode == GEMM_TRSM_PANEL) return p.count * (p.b / BM) * (p.trsm_oop ? p.b / BN : 1);
   if (p.mode == GEMM_CHOL_TRAIL && p.trsm_next)
     return (int64_t)(p.T - p.J - 2) * (p.b / BM) * (p.trsm_par ? p.b / BN : 1);
+  if (p.mode == GEMM_LIST && p.trsm_next) return p.trsm_count * (p.b / BM) * (p.trsm_par ? p.b / BN : 1);
   if (p.mode == GEMM_RECT_TRAIL && p.trsm_next) return (int64_t)p.Tm * (p.b / BM);
   return 0;
 }
 // a trailing update with the next panel's solve appended as gated tasks
 __host__ __device__ __forceinline__ bool gemm_fused_trsm(const GemmProblem& p) {
-  return (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_RECT_TRAIL) && p.trsm_next;
+  return (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_RECT_TRAIL || p.mode == GEMM_LIST) && p.trsm_next;
 }
 // Queue position of the fused TRSM tasks in a trailing-update launch: after
 // every block of tile column J+1 (their inputs) and early enough that the
@@ -186,7 +141,8 @@ __host__ __device__ __forceinline__ int64_t gemm_trsm_pos(const GemmProblem& p) 
   const int64_t nupd = gemm_num_items(p);
   // blocks of the tiles the solve reads: tile column J+1 (Cholesky) or row
   // block J+1 of the transposed right-hand side (kriging solve)
-  const int64_t col = (int64_t)(p.mode == GEMM_RECT_TRAIL ? p.Tm : p.T - p.J - 1) * (p.b / BM) * (p.b / BN);
+  const int64_t col_tiles = p.mode == GEMM_RECT_TRAIL ? p.Tm : (p.mode == GEMM_LIST ? p.col_items : p.T - p.J - 1);
+  const int64_t col = col_tiles * (p.b / BM) * (p.b / BN);
   const int64_t pos = nupd - p.trsm_tail;
   return pos > col ? pos : (col < nupd ? col : nupd);
 }
@@ -250,11 +206,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   it.lower = 0;
   it.bTriRow = -1;
   it.kstages = 0;
-#ifdef BGP_EXP_STORE_EPI  // probe build: updates stored instead of reduced (wrong results; timing only)
-  it.store = 1;
-#else
   it.store = (p.beta == 0.0);
-#endif
   it.bLinv = 0;
   it.gate = -1;
   it.slab = -1;
@@ -262,17 +214,17 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   int64_t idx;
   if (gemm_task_kind(p, task, idx)) {
     // standalone panel, or the fused TRSM of panel J+1 (tiles J+2 .. T-1)
-    if ((p.mode == GEMM_TRSM_PANEL && p.trsm_oop) || (p.mode == GEMM_CHOL_TRAIL && p.trsm_par)) {
+    if ((p.mode == GEMM_TRSM_PANEL && p.trsm_oop) || gemm_par_passes(p)) {
       pass = (int)(idx % nbn);  // one pass per task, right to left within a slab
       idx /= nbn;
-      if (p.mode == GEMM_CHOL_TRAIL) {
+      if (gemm_par_passes(p)) {
         it.slab = (int)idx;
         it.pass = pass;
       }
     }
-    const int64_t panel0 = p.mode == GEMM_TRSM_PANEL   ? p.panel0
-                           : p.mode == GEMM_RECT_TRAIL ? (int64_t)(p.J + 1) * p.Tm
-                                                       : tri_index(p.J + 2, p.J + 1, p.T);
+    const int64_t panel0 = (p.mode == GEMM_TRSM_PANEL || p.mode == GEMM_LIST) ? p.panel0
+                           : p.mode == GEMM_RECT_TRAIL                       ? (int64_t)(p.J + 1) * p.Tm
+                                                                             : tri_index(p.J + 2, p.J + 1, p.T);
     trsm_block(it, p, idx, pass, panel0);
     return it;
   }
@@ -324,12 +276,16 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
       it.bTriRow = I;
       break;
     }
-    default: {  // GEMM_LIST: (C, A, B, lower) tile-index quadruples
+    default: {  // GEMM_LIST: (C, A, B, flags) tile-index quadruples
+      // flags: bit 0 the C tile is a diagonal tile (lower part only); bits
+      // 8.. gate + 1 (0: none): the column-(J+1) tiles of a distributed
+      // sweep step, gate 0 the diagonal tile, 1.. the rank's panel tiles
       const int32_t* q = p.items + 4 * t;
       it.cTile = q[0];
       it.aTile0 = q[1];
       it.bTile0 = q[2];
-      if (q[3]) diag_block(it, bi, bj);
+      if (q[3] & 1) diag_block(it, bi, bj);
+      if (p.col_gate) it.gate = (q[3] >> 8) - 1;
       break;
     }
   }
@@ -338,19 +294,22 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
-  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) &&
-          !(p.mode == GEMM_CHOL_TRAIL && p.trsm_par))
+  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) && !gemm_par_passes(p))
              ? p.b / BN
              : 1;
 }
 
 // spin (acquire, exponential back-off, bounded) until *flag >= need or the
-// factorization failed; returns false on failure / timeout
-__device__ __forceinline__ bool wait_count(const int* flag, int need, const unsigned long long* info) {
+// factorization failed; returns false on failure / timeout.  A timeout is a
+// dependency bug, not data: it is recorded in the status (host: an error).
+__device__ __forceinline__ bool wait_count(const int* flag, int need, unsigned long long* info) {
   unsigned ns = 32;
   for (long long spins = 0; ld_acquire_gpu(flag) < need; ++spins) {
     if (info && *(volatile const unsigned long long*)info != 0ull) return false;
-    if (spins > (1ll << 24)) return false;
+    if (spins > (1ll << 24)) {
+      if (info) atomicCAS(info, 0ull, BGP_INFO_DATAFLOW_TIMEOUT);
+      return false;
+    }
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
   }
@@ -408,19 +367,18 @@ __device__ __forceinline__ uint64_t* stagger_bar(uint8_t* smem) {
   return reinterpret_cast<uint64_t*>(smem + GROUPS * GROUP_BYTES) + GROUPS * 2 * STAGES;
 }
 
+// tmT: the C tiles with the operand box -- the A operand of an in-place TRSM
+// block (the tile it solves), which differs from tmA when A / B are a panel
+// buffer (the distributed sweep step)
 __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtensorMap* tmA,
                                               const CUtensorMap* tmB, const CUtensorMap* tmL,
-                                              const CUtensorMap* tmC, const GemmProblem& p,
-                                              const unsigned long long* info, uint64_t* stagger) {
+                                              const CUtensorMap* tmT, const GemmProblem& p,
+                                              unsigned long long* info, uint64_t* stagger) {
   prefetch_tmap(tmA);
   prefetch_tmap(tmB);
   prefetch_tmap(tmL);
-  prefetch_tmap(tmC);
-#ifdef BGP_EXP_EVICT_NORMAL
-  const uint64_t pol_keep = l2_policy_evict_normal();
-#else
+  prefetch_tmap(tmT);
   const uint64_t pol_keep = l2_policy_evict_last();
-#endif
   const int kc_per_tile = p.b / BK;
   const int64_t ntasks = gemm_num_tasks(p);
   int stage = 0;
@@ -433,13 +391,13 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       // fused TRSM of panel J+1: the tile's update blocks have retired and
       // (Cholesky) the look-ahead CTA published Linv(J+1); the kriging solve's
       // inverses are computed up front (no flag)
-      const int per_tile = (p.b / BM) * ((p.mode == GEMM_CHOL_TRAIL && p.trsm_par) ? p.b / BN : 1);
+      const int per_tile = (p.b / BM) * (gemm_par_passes(p) ? p.b / BN : 1);
       const int tile = (int)(idx / per_tile);
       if (stagger) {  // group 0: release group 1 before blocking (see consumer_loop)
         mbar_arrive(stagger);
         stagger = nullptr;
       }
-      const int g0 = p.mode == GEMM_CHOL_TRAIL ? 1 : 0;  // Cholesky gate 0 is the diagonal tile
+      const int g0 = p.mode == GEMM_RECT_TRAIL ? 0 : 1;  // Cholesky gate 0 is the diagonal tile
       if (!wait_count(p.col_gate + g0 + tile, p.tile_need, info) ||
           (p.linv_flag && !wait_count(p.linv_flag, p.linv_need, info)))
         break;
@@ -450,6 +408,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       const Item it = gemm_decode(p, task, pass);
       if (!it.valid) continue;
       const CUtensorMap* tb = it.bLinv ? tmL : tmB;
+      const CUtensorMap* ta = (it.bLinv && !p.trsm_oop) ? tmT : tmA;
       const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&gs.empty[stage], phase ^ 1);
@@ -466,9 +425,6 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
           sl.slab = it.slab;
           sl.pass = it.pass;
         }
-#ifdef BGP_EXP_NO_TMA  // probe build: consumers run on stale stage data
-        mbar_arrive(&gs.full[stage]);
-#else
         mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
         const int kt = kc / kc_per_tile;
         const int kin = (kc % kc_per_tile) * BK;
@@ -479,11 +435,10 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
         uint8_t* sb = sa + STAGE_A_BYTES;
 #pragma unroll
         for (int i = 0; i < BM / 16; ++i)
-          tma_load_3d(sa + i * BOX_BYTES, tmA, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
+          tma_load_3d(sa + i * BOX_BYTES, ta, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
 #pragma unroll
         for (int i = 0; i < BN / 16; ++i)
           tma_load_3d(sb + i * BOX_BYTES, tb, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
-#endif
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -643,21 +598,13 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   // 0's producer is about to wait on a gate, so group 1 never waits on a
   // group that itself waits (the gated work may be group 1's own).
   bool stagger_arrive = (g == 0 && gwarp == 0);
-#ifndef BGP_EXP_NO_STAGGER
   if (g == 1) mbar_wait(stagger, 0);
-#endif
-#ifdef BGP_EXP_TRACE
-  int t_idx = 0;
-#endif
 
   for (;;) {
     mbar_wait(&gs.full[stage], phase);  // first stage of the next block (or the sentinel)
     const BlockSlot it = gs.slot[stage];
     if (!it.valid) break;
     const int nk = it.nk;
-#ifdef BGP_EXP_LTRACE
-    if (gwarp == 0 && lane == 0 && p.mode == GEMM_CHOL_TRAIL && it.store) LT_MIN(3);
-#endif
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -671,10 +618,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     // is released once its last DMMA issued (fragments in registers) -- except
     // the block's last stage under EPI_IN_STAGE, which holds epilogue rows
     // until release_held() early in the next block.
-#ifdef BGP_EXP_TRACE
-    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-      g_trace[blockIdx.x][g][t_idx][0] = clock64();
-#endif
     Frag f[2];
     uint32_t sb = (uint32_t)stage * STAGE_BYTES;
     load_frag<0>(f[0], offA[0][0] + sb, offA[1][0] + sb, offB[0][0] + sb, offB[1][0] + sb);
@@ -691,13 +634,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         phase ^= 1;
       }
       sb = (uint32_t)stage * STAGE_BYTES;
-#ifdef BGP_EXP_STRACE
-      if (gwarp == 0 && lane == 0 && t_idx < 64 && kc < 19 && blockIdx.x < 148 && g < 2)
-        g_strace[blockIdx.x][g][t_idx][kc] = clock64();
-#endif
-#ifndef BGP_EXP_NO_STAGE_WAIT  // probe build (with NO_TMA): no per-stage wait
       mbar_wait(&gs.full[stage], phase);
-#endif
       load_frag<0>(f[0], offA[0][0] + sb, offA[1][0] + sb, offB[0][0] + sb, offB[1][0] + sb);
       mma_frag(acc, f[(HALVES - 1) & 1]);
       __syncwarp();
@@ -710,10 +647,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       // every warp of the group has read its fragments out of the last
       // stage before any warp overwrites it with epilogue rows
       named_bar_sync(3 + g, 32 * GROUP_WARPS);
-#ifdef BGP_EXP_TRACE
-      if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-        g_trace[blockIdx.x][g][t_idx][3] = clock64();
-#endif
     } else {
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[stage]);
@@ -734,10 +667,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         __threadfence();
         atomicAdd(pd + it.pass, 1);
         for (int q = 0; q < it.pass; ++q)
-          if (!wait_count(pd + q, GROUP_WARPS, info)) {
-            if (info) atomicCAS(info, 0ull, BGP_INFO_DATAFLOW_TIMEOUT);
-            break;
-          }
+          if (!wait_count(pd + q, GROUP_WARPS, info)) break;
       }
       __syncwarp();
     }
@@ -749,48 +679,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     // no read-modify-write on the critical path.  Stores (beta = 0, TRSM
     // blocks): TMA store of acc.  A round waits only until the previous
     // round's boxes were read out of shared memory.
-#ifdef BGP_EXP_TRACE
-    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-      g_trace[blockIdx.x][g][t_idx][1] = clock64();
-#endif
-#ifdef BGP_EXP_NO_EPI  // probe build: no epilogue
-    {
-      double sum = 0.0;
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) sum += acc[i][j][0] + acc[i][j][1];
-      if (sum == 12345.678) gs.cbuf[0] = 1;
-    }
-    continue;
-#endif
-#ifdef BGP_EPI_RED
-    {
-      // straight from registers: red.global.add of -acc (updates) or plain
-      // stores (beta = 0 / TRSM) into the tile, no staging and no waits
-      double* ct = p.cbase + (int64_t)it.cTile * p.b * p.b;
-#pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int m = it.mrow0 + wm * WM + i * 8 + q;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int n = it.nrow0 + wn * WN + j * 8 + 2 * s4 + e;
-            if (it.lower && m < n) continue;  // strict upper triangle stays
-            double* a = ct + (int64_t)n * p.b + m;
-            if (it.store) *a = acc[i][j][e];
-            else asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(-acc[i][j][e]) : "memory");
-          }
-        }
-      }
-    }
-    if (it.gate >= 0) {
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(p.col_gate + it.gate, 1);
-    }
-#else
 #pragma unroll
     for (int r = 0; r < EPI_ROUNDS; ++r) {
       // rounds 0 .. EPI_ROUNDS-2 go to the warp's quarter of the last stage
@@ -816,10 +704,6 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         case 2: stage_round<2>(acc, cb, m0, n0, it.store, it.lower); break;
         default: stage_round<3>(acc, cb, m0, n0, it.store, it.lower); break;
       }
-#ifdef BGP_EXP_TRACE
-      if (r == 0 && gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-        g_trace[blockIdx.x][g][t_idx][4] = clock64();
-#endif
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -837,16 +721,10 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
             tma_reduce_add_3d(tmC, wbuf + b2 * WBOX_BYTES, r0 + b2 * 16, c0, (int)it.cTile, pol_stream);
         }
         tma_store_commit();
-#ifdef BGP_EXP_TRACE
-        if (r == 0 && gwarp == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-          g_trace[blockIdx.x][g][t_idx][5] = clock64();
-#endif
       }
     }
     store_pending = true;
     if constexpr (EPI_IN_STAGE) held = last;
-#endif
-#ifndef BGP_EPI_RED
     // Column-(J+1) gates: a warp signals a block once its bulk reduction has
     // retired (completion, proxy fence, release).  Not deferred: this group's
     // own producer may be the one waiting for the tile.
@@ -859,43 +737,23 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       }
       __syncwarp();
     }
-#endif
-#ifdef BGP_EXP_LTRACE
-    if (gwarp == 0 && lane == 0 && p.mode == GEMM_CHOL_TRAIL) {
-      if (it.store) LT_MAX(4);
-      else LT_MAX(5);
-    }
-#endif
-#ifdef BGP_EXP_TRACE
-    if (gwarp == 0 && lane == 0 && t_idx < TRACE_ITEMS && blockIdx.x < 148)
-      g_trace[blockIdx.x][g][t_idx][2] = clock64();
-    ++t_idx;
-#endif
   }
   if (stagger_arrive && lane == 0) mbar_arrive(stagger);
   release_held();
   if (lane == 0 && store_pending) tma_store_wait_all0();
   if (p.npush > 0) __threadfence_system();  // pushed panel visible to the peers
-#ifdef BGP_EXP_LTRACE
-  if (lane == 0 && p.mode == GEMM_CHOL_TRAIL) LT_MAX(6);
-#endif
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ CUtensorMap tmT,
                      const GemmProblem p, unsigned long long* __restrict__ info,
                      const __grid_constant__ PushMaps pm) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ int s_go;
+  __shared__ int s_go, s_role;
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // 128B swizzle needs 1 KB alignment
   if (info && *(volatile const unsigned long long*)info != 0ull) return;  // factorization failed
-#ifdef BGP_EXP_LTRACE
-  if (threadIdx.x == 0 && p.mode == GEMM_CHOL_TRAIL) {
-    LT_MIN(0);
-    if (blockIdx.x == 0) g_ltrace[p.trace_slot & 8191][7] = p.T;
-  }
-#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wg = warp >> 2;
@@ -909,20 +767,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(stagger_bar(smem), 1);
     fence_barrier_init();
+    // look-ahead role: the first CTA to start takes it (a CTA that is running
+    // for sure -- a fixed block index might only be scheduled once others
+    // exit, and those may be waiting for the inverse it publishes)
+    s_role = p.potrf_tile != nullptr && atomicAdd(p.role_ticket, 1) == 0;
   }
   __syncthreads();
   // look-ahead CTA: factor (and invert) the next panel's diagonal tile first
-  const bool lookahead_cta = p.potrf_tile != nullptr && blockIdx.x == gridDim.x - 1;
+  const bool lookahead_cta = s_role != 0;
 
   if (wg == 0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (lookahead_cta) named_bar_sync(1, THREADS);  // wait for the panel work below
-#ifdef BGP_EXP_ONE_GROUP  // probe build: only consumer group 0 works (single-warp-per-SMSP rate)
-    if (warp < 1 && lane == 0)
-#else
     if (warp < GROUPS && lane == 0)
-#endif
-      producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmC, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
+      producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmT, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     if (lookahead_cta) {
@@ -933,15 +791,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (ctid < 256) {
         double* psm = reinterpret_cast<double*>(smem);
         if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
-#ifdef BGP_EXP_LTRACE
-        if (ctid == 0) LT_SET(1);
-#endif
         named_bar_sync(2, 256);
         const bool la_ok = s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
                                                         p.trsm_next ? p.linv : nullptr, psm, ctid, 2);
-#ifdef BGP_EXP_LTRACE
-        if (ctid == 0) LT_SET(2);
-#endif
         if (la_ok && p.trsm_next) {
           __threadfence();
           named_bar_sync(2, 256);
@@ -951,9 +803,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       named_bar_sync(1, THREADS);  // release this CTA's producers
     }
     const int g = wg - 1;
-#ifdef BGP_EXP_ONE_GROUP
-    if (g != 0) return;
-#endif
     consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm, info);
   }
 }
@@ -991,20 +840,27 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   const int64_t tasks = gemm_num_tasks(p);
   if (tasks <= 0) return BGP_OK;
   int rc;
-  if (!p.queue) {  // a zeroed task counter of the context's own
-    if ((rc = ensure(ctx, (void**)&ctx->d_queue, &ctx->queue_cap, 256))) return rc;
-    cudaError_t e = cudaMemsetAsync(ctx->d_queue, 0, 8, s);
+  if (!p.queue || (p.potrf_tile && !p.role_ticket)) {
+    // a zeroed task counter (+ look-ahead ticket) of this launch's own: slot
+    // k of a ring, zeroed on the launch's stream.  Launches on one stream
+    // are ordered; launches on different streams (the caller's overlap)
+    // never share a slot unless QUEUE_RING launches are in flight at once.
+    if ((rc = ensure(ctx, (void**)&ctx->d_queue_ring, &ctx->queue_ring_cap, Ctx::QUEUE_RING * 16))) return rc;
+    int* slot = ctx->d_queue_ring + 4 * (ctx->queue_next++ % Ctx::QUEUE_RING);
+    cudaError_t e = cudaMemsetAsync(slot, 0, 16, s);
     if (e != cudaSuccess) return set_err(ctx, "gemm queue reset", e);
-    p.queue = ctx->d_queue;
+    if (!p.queue) p.queue = slot;
+    if (!p.role_ticket) p.role_ticket = slot + 2;
   }
-  CUtensorMap mA, mB, mL, mC;
+  CUtensorMap mA, mB, mL, mC, mT;
   if ((rc = make_tile_map(ctx, &mA, Abase, p.b, nA, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mB, Bbase, p.b, nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mL, Linv ? Linv : Bbase, p.b, Linv ? 1 : nB, 16, BK, true)) != BGP_OK) return rc;
   if ((rc = make_tile_map(ctx, &mC, Cbase, p.b, nC, 16, WN, true)) != BGP_OK) return rc;
+  if ((rc = make_tile_map(ctx, &mT, Cbase, p.b, nC, 16, BK, true)) != BGP_OK) return rc;
   PushMaps pm;
   memset(&pm, 0, sizeof(pm));
-  if (p.npush < 0 || p.npush > BGP_MAX_PUSH || (p.npush > 0 && p.mode != GEMM_TRSM_PANEL))
+  if (p.npush < 0 || p.npush > BGP_MAX_PUSH || (p.npush > 0 && p.mode != GEMM_TRSM_PANEL && p.mode != GEMM_LIST))
     return set_err(ctx, "gemm: bad push destinations", cudaErrorInvalidValue);
   for (int d = 0; d < p.npush; ++d)
     if ((rc = make_tile_map(ctx, &pm.map[d], p.push_dst[d], p.b, p.push_tiles, 16, WN, true)) != BGP_OK) return rc;
@@ -1015,81 +871,24 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   // the look-ahead CTA's device POTRF / inverse must fit the ring memory
   if (p.potrf_tile && tile_potrf_inv_smem_bytes(p.b, true) > (size_t)(GROUPS * GROUP_BYTES))
     return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
-  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, p,
+  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, mT, p,
                                                                   p.check_info ? ctx->d_info : nullptr, pm);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");
 }
 
-}  // namespace BGP_GEMM_NS
-
-#ifndef BGP_GEMM_SECONDARY
-namespace bk32 {
-void prepare();
-int launch(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA, const double* Bbase,
-           int64_t nB, int64_t nC, cudaStream_t s, const double* Linv);
-int tile_blocks(int b);
-int diag_blocks(int b);
-int block_warps();
-int groups();
-}  // namespace bk32
-
-static bool use_bk32(int b) {
-  static const int force = [] {  // BGP_GEMM_CFG=16 / 32 (diagnostics): one configuration everywhere
-    const char* e = getenv("BGP_GEMM_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  (void)b;
-  return force != 16;
-}
+}  // namespace dmma
 
 void gemm_block_counts(int b, int* tile_need, int* diag_need, int* groups_per_cta) {
-  if (use_bk32(b)) {
-    *tile_need = bk32::tile_blocks(b) * bk32::block_warps();
-    *diag_need = bk32::diag_blocks(b) * bk32::block_warps();
-    *groups_per_cta = bk32::groups();
-  } else {
-    *tile_need = bk16::tile_blocks(b) * bk16::block_warps();
-    *diag_need = bk16::diag_blocks(b) * bk16::block_warps();
-    *groups_per_cta = bk16::groups();
-  }
+  *tile_need = dmma::tile_blocks(b) * dmma::block_warps();
+  *diag_need = dmma::diag_blocks(b) * dmma::block_warps();
+  *groups_per_cta = dmma::groups();
 }
 
-void gemm_prepare() {
-  bk16::prepare();
-  bk32::prepare();
-}
+void gemm_prepare() { dmma::prepare(); }
 
-// Every tile size runs the BK = 32 configuration (half the barrier and TMA
-// operations per DMMA, epilogue staged in the last stage).  Measured on C4:
-// b = 512 +0.9 % over BK = 16 (before the in-stage epilogue), b = 256 +3.0 %
-// (with it; -1.7 % before).  BGP_GEMM_CFG=16 (diagnostics) forces BK = 16.
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,
                 const double* Bbase, int64_t nB, int64_t nC, cudaStream_t s, const double* Linv) {
-  if (use_bk32(p.b)) return bk32::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
-  return bk16::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
+  return dmma::launch(ctx, p, Cbase, Abase, nA, Bbase, nB, nC, s, Linv);
 }
-#endif
 }  // namespace bgp
-
-#if defined(BGP_EXP_TRACE) && !defined(BGP_GEMM_SECONDARY)
-extern "C" int bgp_probe_trace(void* host_out) {
-  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_trace, sizeof(bgp::bk16::g_trace));
-}
-#endif
-#if defined(BGP_EXP_LTRACE) && defined(BGP_GEMM_SECONDARY)
-extern "C" int bgp_probe_ltrace(void* host_out, int reset) {
-  if (reset) {
-    static unsigned long long init[8192][8];
-    for (int i = 0; i < 8192; ++i)
-      for (int k = 0; k < 8; ++k) init[i][k] = (k == 0 || k == 3) ? ~0ull : 0ull;
-    return (int)cudaMemcpyToSymbol(bgp::bk32::g_ltrace, init, sizeof(init));
-  }
-  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk32::g_ltrace, sizeof(bgp::bk32::g_ltrace));
-}
-#endif
-#if defined(BGP_EXP_STRACE) && !defined(BGP_GEMM_SECONDARY)
-extern "C" int bgp_probe_strace(void* host_out) {
-  return (int)cudaMemcpyFromSymbol(host_out, bgp::bk16::g_strace, sizeof(bgp::bk16::g_strace));
-}
-#endif

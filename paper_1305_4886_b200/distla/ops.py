@@ -46,10 +46,12 @@ def _need(ctx, name, kind, full=True):
     return _full(ctx, obj) if full else obj
 
 
-def _packed_index(dist):
+def _packed_index(dist, tiles=None):
+    """Packed-triangle index of a rank's tiles (default: the owned ones)."""
     import torch
-    I = dist.tiles[:, 0].astype(np.int64)
-    J = dist.tiles[:, 1].astype(np.int64)
+    tiles = dist.tiles if tiles is None else tiles
+    I = tiles[:, 0].astype(np.int64)
+    J = tiles[:, 1].astype(np.int64)
     T = dist.T
     return torch.from_numpy(J * T - J * (J - 1) // 2 + (I - J))
 
@@ -203,10 +205,11 @@ def construct(ctx, name, kind, generator, params, inputs_name, row_layout, col_l
     if kind == "triangular" and ctx.G > 1:
         from ..parallel import TileDist
         td = TileDist(n, ctx.tile, ctx.grid, ctx.rank - 1)
-        out = ctx.empty((max(td.count, 1), ctx.tile, ctx.tile))
-        tij = ctx.upload_int32(td.tiles)
+        # owned tiles, then the shadow diagonal tiles (parallel.TileDist)
+        out = ctx.empty((max(td.storage_count, 1), ctx.tile, ctx.tile))
+        tij = ctx.upload_int32(td.storage_tiles)
         ctx.call("bgp_construct_tiles", ctypes.byref(desc), _ptr(X) if X is not None else None, n, dim,
-                 ctx.tile, _ptr(tij), td.count, _ptr(out), ctx.stream)
+                 ctx.tile, _ptr(tij), td.storage_count, _ptr(out), ctx.stream)
         ctx.store[name] = DevObj(kind, row_layout, col_layout or row_layout, ctx.tile, out, td)
         ctx.log_event("construct")
         return
@@ -246,7 +249,7 @@ def split(ctx, name, kind, array, row_layout, col_layout=None):
     if kind == "triangular" and ctx.G > 1:
         from ..parallel import TileDist
         td = TileDist(n, ctx.tile, ctx.grid, ctx.rank - 1)
-        out = out.index_select(0, _packed_index(td).to(out.device)).contiguous()
+        out = out.index_select(0, _packed_index(td, td.storage_tiles).to(out.device)).contiguous()
     ctx.store[name] = DevObj(kind, row_layout, cl, ctx.tile, out, td)
 
 
@@ -285,7 +288,9 @@ def cholesky(ctx, name, out_name):
         ctx.store.pop(out_name, None)
         raise NotPositiveDefinite((info.value - 1) // obj.row_layout.block_size + 1)
     ctx.log_event("factor")
-    nt = obj.dist.count if obj.dist is not None else obj.data.shape[0]
+    if obj.dist is not None:  # owned tiles, and the shadow diagonal tiles held besides
+        return {"peak_blocks": obj.dist.storage_count, "owned_blocks": obj.dist.count, "tile": obj.tile}
+    nt = obj.data.shape[0]
     return {"peak_blocks": nt, "owned_blocks": nt, "tile": obj.tile}
 
 
@@ -404,8 +409,10 @@ def xprod_self_diag(ctx, v_name, out_name):
 def logdet(ctx, l_name):
     L = _need(ctx, l_name, "triangular", full=False)
     if L.dist is not None:
-        from ..parallel import dist_logdet
-        value, info = dist_logdet(L.dist, L.data, _tile_ops(ctx, L.n), ctx.comm)
+        # this rank's partial over its diagonal tiles; run() gathers the
+        # partials and the master sums them in rank order (__init__.py:157)
+        value, info = _tile_ops(ctx, L.n).logdet_partial(L.data, L.dist.diag_items())
+        info = ctx.comm.min_nonzero(info)
         if info:
             raise SingularDiagonal(f"non-positive diagonal at row {info}")
         return value
@@ -421,6 +428,8 @@ def logdet(ctx, l_name):
 @registry.register("distla.sumsq")
 def sumsq(ctx, name):
     x = _need(ctx, name, "vector")
+    if ctx.G > 1 and ctx.rank != 1:
+        return 0.0  # vectors are replicated: rank 1 holds the whole sum
     out = ctypes.c_double(0.0)
     ctx.call("bgp_sumsq", _ptr(x.data), x.n, ctypes.byref(out), ctx.stream)
     return out.value

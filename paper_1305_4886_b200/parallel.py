@@ -8,10 +8,11 @@ Replaces the reference's triangular D(D+1)/2 process fold
     Pr x Pc grid (1x1, 1x2, 2x2, 2x4); a rank stores its tiles packed by
     tile column, so each owned part of a panel is contiguous;
   * construct: every rank generates only its own tiles (no communication);
-  * Cholesky step J: the owner of (J, J) factors it and broadcasts L_JJ; the
-    ranks of process column J mod Pc solve their panel tiles; every process
-    row's panel chunk is broadcast to all ranks; each rank applies the
-    DMMA trailing update to its own tiles (bgp_tile_update, tile-list mode);
+  * Cholesky step J: ONE launch per rank (bgp_dist_step) updates the rank's
+    tiles with panel J; on process column (J+1) mod Pc the same launch
+    factors (J+1, J+1) (the owner's tile or a shadow copy), solves the
+    rank's panel-(J+1) tiles and stores them into every rank's panel buffer
+    over NVLink; a stream-ordered barrier separates the steps (dist_cholesky);
   * forward / back solve: per block, the partial products of the owners of
     row (column) J are reduced to the diagonal owner, which solves and
     broadcasts x_J (2 x b doubles of traffic per step);
@@ -20,7 +21,7 @@ Replaces the reference's triangular D(D+1)/2 process fold
 
 The schedule below is written against two small interfaces so the same code
 runs on the GPUs (`LibTileOps` over libbgp + NCCL) and in the CPU tests
-(a numpy tile backend + gloo, world size 2).
+(a numpy tile backend + gloo, world sizes 2, 4 and 8).
 """
 
 from dataclasses import dataclass, field
@@ -31,8 +32,37 @@ from .grid import DeviceGrid
 
 
 @dataclass
+class StepPlan:
+    """What one rank does in step J of the sweep (one launch, bgp_dist_step).
+
+    items: (C local, A slot, B slot, flags) int32, column J+1 first
+      (col_items of them); flags bit 0 = diagonal tile, bits 8.. = gate + 1.
+    diag: local index of the tile (J+1, J+1) this rank factors in the launch
+      (its own, or its shadow copy), or -1.
+    trsm: (first local index, count) of its panel-(J+1) tiles, solved in the
+      launch once their gates and the inverse are in.
+    """
+
+    items: np.ndarray
+    col_items: int
+    diag: int
+    diag_row0: int
+    trsm: tuple
+
+
+@dataclass
 class TileDist:
-    """Ownership map of the lower tiles of an n x n matrix for one rank."""
+    """Ownership map of the lower tiles of an n x n matrix for one rank.
+
+    Besides the tiles it owns, a rank keeps SHADOW copies of the diagonal
+    tiles (K, K) of its process column owned by the other process row, for
+    every K whose panel has tiles on this rank.  A shadow receives the same
+    updates as the owner's tile (every panel is on every rank), so each rank
+    of process column K mod Pc factors and inverts (K, K) itself inside its
+    step launch and no rank ever waits on another inside a kernel.  Storage:
+    owned tiles packed by tile column at [0, count), shadows at
+    [count, count + len(shadows)).
+    """
 
     n: int
     b: int
@@ -43,6 +73,8 @@ class TileDist:
     local: dict = field(init=False)            # (I, J) -> local tile index
     col_start: np.ndarray = field(init=False)  # first local index of column J
     col_count: np.ndarray = field(init=False)
+    shadows: list = field(init=False)          # K of the shadow diagonal tiles
+    shadow_local: dict = field(init=False)     # K -> local index of the shadow
 
     def __post_init__(self):
         self.T = -(-self.n // self.b)
@@ -58,10 +90,24 @@ class TileDist:
         for I, J in tl:
             self.col_count[J] += 1
         self.col_start[1:] = np.cumsum(self.col_count)
+        self.shadows = [K for K in range(T) if K % pc == r_col and K % pr != r_row
+                        and self.my_panel(K)[1] > 0]
+        self.shadow_local = {K: len(tl) + i for i, K in enumerate(self.shadows)}
 
     @property
     def count(self):
         return len(self.tiles)
+
+    @property
+    def storage_count(self):
+        """Local tiles including the shadow diagonal tiles."""
+        return len(self.tiles) + len(self.shadows)
+
+    @property
+    def storage_tiles(self):
+        """(I, J) of every local tile, shadows last (what construct builds)."""
+        sh = np.array([(K, K) for K in self.shadows], dtype=np.int32).reshape(-1, 2)
+        return np.concatenate([self.tiles, sh]).astype(np.int32)
 
     def owner(self, I, J):
         return self.grid.owner(I, J)
@@ -95,15 +141,52 @@ class TileDist:
             return s + 1, c - 1
         return s, c
 
+    def factor_tile(self, K):
+        """Local index of the (K, K) copy this rank factors, or -1: the owner
+        always factors its tile; another rank of process column K mod Pc
+        factors its shadow when it holds panel-K tiles to solve."""
+        k = self.local.get((K, K))
+        if k is not None:
+            return k
+        return self.shadow_local.get(K, -1)
+
     def update_items(self, J, slot):
-        """(C local, A slot, B slot, lower) for my tiles (R, C), J < C <= R."""
+        """(C local, A slot, B slot, lower) for my tiles (R, C), J < C <= R,
+        and my shadows (K, K), K > J."""
         first = int(self.col_start[J + 1]) if J + 1 <= self.T - 1 else self.count
         t = self.tiles[first:]
-        if len(t) == 0:
+        rows = []
+        if len(t):
+            R, C = t[:, 0].astype(np.int64), t[:, 1].astype(np.int64)
+            rows.append(np.stack([np.arange(first, first + len(t)), slot[R], slot[C], (R == C)], axis=1))
+        sh = [(self.shadow_local[K], slot[K], slot[K], 1) for K in self.shadows if K > J]
+        if sh:
+            rows.append(np.array(sh, dtype=np.int64))
+        if not rows:
             return np.zeros((0, 4), dtype=np.int32)
-        R, C = t[:, 0].astype(np.int64), t[:, 1].astype(np.int64)
-        items = np.stack([np.arange(first, first + len(t)), slot[R], slot[C], (R == C)], axis=1)
-        return items.astype(np.int32)
+        return np.concatenate(rows).astype(np.int32)
+
+    def step_plan(self, J, slot):
+        """StepPlan of step J: the update by panel J of every local tile of
+        columns > J (column J+1 first, gated), and, on process column
+        (J+1) mod Pc, the factorization of (J+1, J+1) and the solve of this
+        rank's panel-(J+1) tiles inside the same launch."""
+        K = J + 1
+        items = self.update_items(J, slot)
+        d = self.factor_tile(K)
+        s, c = self.my_panel(K)
+        if d < 0:
+            return StepPlan(items, 0, -1, K * self.b, (s, 0))
+        gate = np.full(len(items), -1, dtype=np.int64)
+        gate[items[:, 0] == d] = 0
+        for t in range(c):
+            gate[items[:, 0] == s + t] = 1 + t
+        items = items.copy()
+        col = gate >= 0
+        items[col, 3] |= ((gate[col] + 1) << 8).astype(np.int32)
+        order = np.concatenate([np.nonzero(col)[0][np.argsort(gate[col], kind="stable")],
+                                np.nonzero(~col)[0]])
+        return StepPlan(items[order], int(col.sum()), d, K * self.b, (s, c))
 
     def diag_items(self):
         """(local index, J) of my diagonal tiles."""
@@ -122,71 +205,64 @@ class TileDist:
         return np.array(sel, dtype=np.int32).reshape(-1, 2)
 
 
+# steps whose update work (tiles) is below this run the fused TRSM's column
+# passes as independent tasks (the chain-bound regime; capi.cu bgp_potrf)
+_PAR_PASS_TILES = {128: 48 * 49 // 2, 256: 26 * 27 // 2, 384: 22 * 23 // 2, 512: 18 * 19 // 2}
+
+
 def dist_cholesky(dist, local, ops, comm):
-    """Right-looking tiled Cholesky of a distributed matrix, in place, with a
-    one-panel look-ahead.
+    """Right-looking tiled Cholesky of a distributed matrix, in place, with
+    the look-ahead inside each step's launch.
 
-    `local` is this rank's (count, b, b) tile stack.  Returns the first
-    failing pivot row (1-based, LAPACK info) agreed by all ranks, or 0.
+    `local` is this rank's (storage_count, b, b) tile stack (owned tiles,
+    then shadow diagonal tiles).  Returns the first failing pivot row
+    (1-based, LAPACK info) agreed by all ranks, or 0.
 
-    Step J: every rank first updates its tiles of column J+1 with panel J.
-    Then, on the side stream (ops.side()), the owner of (J+1, J+1) factors
-    and inverts it, the inverse is broadcast, process column (J+1) mod Pc
-    solves its panel tiles (A <- A Linv^T on the DMMA GEMM) and the panel
-    reaches every rank -- stored by that same TRSM kernel into every rank's
-    panel buffer over NVLink (PanelExchange), or, as the fallback, broadcast
-    row chunk by row chunk over NCCL -- while the rest of the trailing update
-    (columns >= J+2, panel J) runs on the compute stream on all SMs but a few
-    (ops.update(..., reserve=True)), which the collectives and the small
-    panel kernels use.  ops.join_side() then orders step J+1 after panel J+1.
-    The update items of every step are built and uploaded once, and a failing
-    pivot stays in the device status until the end, so the host never waits
-    on the GPU inside the loop.
+    Step J is ONE launch per rank (ops.step -> bgp_dist_step) on one stream:
+    the update of all its tiles by panel J, column J+1 first; on process
+    column (J+1) mod Pc the launch also factors and inverts (J+1, J+1) --
+    every such rank its own copy (the owner's tile or its shadow), so no
+    kernel waits on another GPU -- and solves the rank's panel-(J+1) tiles
+    as gated tasks, storing each solved block into every rank's panel
+    buffer over NVLink (PanelExchange).  One stream-ordered barrier between
+    step launches orders the exchange: after it, panel J+1 is complete on
+    every rank and every rank has finished reading the buffer that step J+1
+    overwrites (double-buffered panels).  Without peer mappings the panel
+    goes out by NCCL broadcasts after the launch instead (one per process
+    row).  The host enqueues the whole sweep without waiting on the GPU; a
+    failing pivot stays in the device status, which skips later launches.
     """
     b, T, me = dist.b, dist.T, dist.rank
-    inv_buf = ops.empty((b, b))
-    ops.begin()
-    info = [0]
-    panels = [None, None]
+    ops.sweep_begin(T)
     layouts = [dist.panel_layout(J) for J in range(T - 1)]
-    col_items, rest_items = [], []
-    for J in range(T - 1):
-        it = np.asarray(dist.update_items(J, layouts[J][1])).reshape(-1, 4)
-        cols = dist.tiles[it[:, 0], 1] if len(it) else np.zeros(0, dtype=np.int32)
-        col_items.append(it[cols == J + 1])
-        rest_items.append(it[cols != J + 1])
-    dev_col = ops.prepare_items(col_items)
-    dev_rest = ops.prepare_items(rest_items)
-    # fused panel exchange (TRSM epilogue stores into every rank's panel
-    # buffer over NVLink), or None: TRSM then NCCL broadcasts
+    plans = [dist.step_plan(J, layouts[J][1]) for J in range(T - 1)]
+    dev = ops.prepare_items([p.items for p in plans])
+    par_tiles = _PAR_PASS_TILES.get(b, 0)
+    # fused panel exchange (the TRSM epilogue stores into every rank's panel
+    # buffer over NVLink), or None: NCCL broadcasts after each step's launch
     xchg = ops.panel_exchange(comm, T) if hasattr(ops, "panel_exchange") else None
+    panels = [None, None]
 
-    def factor_panel(K):
-        d = dist.owner(K, K)
-        if xchg is not None and K + 1 < T:
-            # every rank is done with buffer K % 2 (its last reader, step K-2's
-            # update, precedes this point on every rank's streams)
-            comm.barrier_stream()
-        if me == d:
-            info[0] = info[0] or ops.potrf_factor(local, dist.local[(K, K)], K * b,
-                                                  inv_buf if K + 1 < T else None)
-        if K + 1 >= T:
-            return
-        comm.broadcast(inv_buf, d)
-        s, c = dist.my_panel(K)
-        chunks, _, ntot = layouts[K]
+    def buffer(K, ntot):
         if xchg is not None:
-            if c:
-                off = next(o for root, o, cnt in chunks if root == me and cnt)
-                xchg.push(inv_buf, local, s, c, K % 2, off)
-            comm.barrier_stream()  # panel K is in every rank's buffer
-            panels[K % 2] = xchg.bufs[K % 2]
-            return
-        if c:
-            ops.trsm_inv(inv_buf, local, s, c)
+            return xchg.bufs[K % 2]
         if panels[K % 2] is None or panels[K % 2].shape[0] < ntot:
             panels[K % 2] = ops.empty((max(ntot, 1), b, b))
-        panel = panels[K % 2]
+        return panels[K % 2]
+
+    def push_args(K):
+        """Destinations of my panel-K tiles: (xchg, which buffer, first slot)."""
+        if xchg is None or K >= T - 1:
+            return None
+        chunks = layouts[K][0]
+        off = next((o for root, o, cnt in chunks if root == me and cnt), 0)
+        return (xchg, K % 2, off)
+
+    def broadcast_panel(K):
+        """Fallback exchange of panel K (after its solve): one broadcast per
+        process-row chunk into every rank's panel buffer."""
+        chunks, _, ntot = layouts[K]
+        panel = buffer(K, ntot)
         for root, off, cnt in chunks:
             if cnt == 0:
                 continue
@@ -197,14 +273,24 @@ def dist_cholesky(dist, local, ops, comm):
                 ops.copy_tiles(view, local, ps, cnt)
             comm.broadcast(view, root)
 
-    factor_panel(0)
+    # panel 0: factor (0, 0) (every rank of process column 0 its own copy),
+    # solve and deliver my panel-0 tiles
+    d0 = dist.factor_tile(0)
+    s0, c0 = dist.my_panel(0)
+    if d0 >= 0:
+        ops.first_panel(local, d0, (s0, c0), push_args(0))
+    if T > 1:
+        if xchg is None:
+            broadcast_panel(0)
     for J in range(T - 1):
-        ops.update(local, panels[J % 2], dev_col[J])
-        with ops.side():
-            factor_panel(J + 1)
-        ops.update(local, panels[J % 2], dev_rest[J], reserve=True)
-        ops.join_side()
-    return comm.min_nonzero(ops.end(info[0]))
+        if xchg is not None:
+            comm.barrier_stream()  # panel J complete everywhere; buffer (J+1) % 2 free
+        plan = plans[J]
+        par = plan.trsm[1] > 0 and len(plan.items) <= par_tiles
+        ops.step(J, local, buffer(J, layouts[J][2]), dev[J], plan, par, push_args(J + 1))
+        if xchg is None and J + 1 < T - 1:
+            broadcast_panel(J + 1)
+    return comm.min_nonzero(ops.end())
 
 
 def dist_trsv(dist, local, y, ops, comm, forward=True):
@@ -395,6 +481,13 @@ class TorchComm:
         self.dist.all_gather_object(out, bytes(value), group=self.group)
         return out
 
+    def all_gather_object(self, value):
+        if self.world == 1:
+            return [value]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, value, group=self.group)
+        return out
+
     def all_gather_float(self, value):
         if self.world == 1:
             return [value]
@@ -567,39 +660,14 @@ class LibTileOps:
     def begin(self):
         self.cl.call("bgp_info_reset", self.cl.stream)
 
-    def end(self, info):
+    def end(self, info=0):
         import ctypes
         dev = ctypes.c_int64(0)
         self.cl.call("bgp_info_read", ctypes.byref(dev), self.cl.stream)
         return int(info or dev.value)
 
-    def potrf_factor(self, local, k, row0, inv):
-        """Factor tile k in place and (inv not None) write its inverse; the
-        status stays on the device until end()."""
-        self.cl.call("bgp_tile_potrf_async", self._p(local[k]), self.b, row0,
-                     self._p(inv) if inv is not None else None, self.cl.stream)
-        return 0
-
-    def potrf(self, local, k, row0):
-        import ctypes
-        info = ctypes.c_int64(0)
-        self.cl.call("bgp_tile_potrf", self._p(local[k]), self.b, row0, ctypes.byref(info),
-                     self.cl.stream)
-        return int(info.value)
-
-    def copy_tile(self, dst, local, k):
-        dst.copy_(local[k])
-
     def copy_tiles(self, dst, local, start, count):
         dst.copy_(local[start:start + count])
-
-    def trsm_inv(self, inv, local, start, count):
-        self.cl.call("bgp_panel_trsm_inv", self._p(inv), self._p(local[start]), count, self.b,
-                     self.cl.stream)
-
-    def trsm(self, diag, local, start, count):
-        self.cl.call("bgp_panel_trsm", self._p(diag), self._p(local[start]), count, self.b,
-                     self.cl.stream)
 
     def prepare_items(self, per_step):
         """Upload the update items of every step at once; returns per-step
@@ -629,43 +697,52 @@ class LibTileOps:
             cache["x"] = x
         return x if x.ok else None
 
-    # SMs left free during a reserved update for the side stream's NCCL
-    # collectives, POTRF and panel solve
-    RESERVE_SMS = 8
+    def sweep_begin(self, T):
+        self._T = T
+        self.cl.call("bgp_dist_begin", T, self.b, self.cl.stream)
+        if getattr(self, "_linv", None) is None:
+            self._linv = self.cl.empty((self.b, self.b))
 
-    def side(self):
-        """Context: run on the side stream, after the work enqueued so far."""
-        import torch
-        if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.cl.device)
-        self._side.wait_stream(torch.cuda.current_stream(self.cl.device))
-        return torch.cuda.stream(self._side)
+    @staticmethod
+    def _dst(push, count):
+        """(dst array, ndst, first slot, buffer tiles) of a panel push."""
+        if push is None or count == 0:
+            return None, 0, 0, 1
+        xchg, which, slot0 = push
+        return xchg.dst[which], len(xchg.dst[which]), slot0, xchg.tiles
 
-    def join_side(self):
-        import torch
-        if getattr(self, "_side", None) is not None:
-            torch.cuda.current_stream(self.cl.device).wait_stream(self._side)
-
-    def update(self, local, panel, items, reserve=False):
-        if isinstance(items, tuple):
-            dev, count = items
-        else:
-            dev, count = self._items(items), len(items)
-        if count == 0:
+    def first_panel(self, local, d, trsm, push):
+        """Factor local tile d (panel 0's diagonal, or its shadow), invert it,
+        solve my panel-0 tiles and (push) deliver them to every rank."""
+        s, c = trsm
+        self.cl.call("bgp_tile_potrf_async", self._p(local[d]), self.b, 0,
+                     self._p(self._linv) if c else None, self.cl.stream)
+        if c == 0:
             return
+        dst, ndst, slot0, tiles = self._dst(push, c)
+        if ndst:
+            self.cl.call("bgp_panel_trsm_push", self._p(self._linv), self._p(local[s]), c, self.b,
+                         dst, ndst, slot0, tiles, self.cl.stream)
+        else:
+            self.cl.call("bgp_panel_trsm_inv", self._p(self._linv), self._p(local[s]), c, self.b,
+                         self.cl.stream)
+
+    def step(self, J, local, panel, items, plan, par, push):
+        """Step J of the sweep on this rank: one bgp_dist_step launch."""
+        dev, count = items
+        s, c = plan.trsm
+        if count == 0 and plan.diag < 0:
+            return
+        dst, ndst, slot0, tiles = self._dst(push, c)
+        diag = self._p(local[plan.diag]) if plan.diag >= 0 else None
+        args = ("bgp_dist_step", J, self._p(local), local.shape[0], self._p(panel), panel.shape[0],
+                self._p(dev) if count else None, count, plan.col_items, diag, plan.diag_row0, s, c,
+                1 if par else 0, dst, ndst, slot0, tiles, self.b, self.cl.stream)
         if self.timeline is not None:
             with self.timeline.span("compute"):
-                self._update(local, panel, dev, count, reserve)
+                self.cl.call(*args)
         else:
-            self._update(local, panel, dev, count, reserve)
-
-    def _update(self, local, panel, dev, count, reserve):
-        if reserve:
-            self.cl.call("bgp_tile_update_limited", self._p(local), self._p(panel), self._p(panel),
-                         self._p(dev), count, self.b, self.cl.num_sms - self.RESERVE_SMS, self.cl.stream)
-        else:
-            self.cl.call("bgp_tile_update", self._p(local), self._p(panel), self._p(panel),
-                         self._p(dev), count, self.b, self.cl.stream)
+            self.cl.call(*args)
 
     def sub_into(self, out, a, b):
         self.cl.call("bgp_sub", self._p(a), self._p(b), self._p(out), out.numel(), self.cl.stream)

@@ -166,19 +166,29 @@ class B200Cluster:
         if self.state != "running":
             raise ClusterDown("cluster has been shut down")
 
-    def run(self, fn_id, **kwargs):
-        """Run a registered operation; returns per-rank results (rank order)."""
+    def run_local(self, fn_id, **kwargs):
+        """Run a registered operation on this rank; returns its own result."""
         self._check_up()
         self.epoch += 1
         self.stats["collectives"] += 1
         fn = registry.lookup(fn_id)
         try:
-            result = fn(self, **kwargs)
+            return fn(self, **kwargs)
         except BlockGPError:
             raise
         except Exception as exc:  # device / driver failures carry rank attribution
             raise WorkerFailure(self.rank, exc) from exc
-        return [result]
+
+    def run(self, fn_id, **kwargs):
+        """Run a registered operation; returns the per-rank results in rank
+        order, one per GPU (bg/transport/base.py:229-234).  With G > 1 (one
+        process per GPU) every rank runs the op and the results of the ops
+        that return per-rank values (stats, partial sums) are all-gathered,
+        so every process sees the same P-length list."""
+        result = self.run_local(fn_id, **kwargs)
+        if self.G == 1:
+            return [result]
+        return per_rank_results(self.comm, fn_id, result, self.G)
 
     def push(self, name, value, targets=None):
         self._check_up()
@@ -222,6 +232,18 @@ class B200Cluster:
         out, self.events = sorted(self.events), []
         return out
 
+    def collect_dense(self, name, diagonal=False):
+        """Unpadded host copy of a device object (distla.collect /
+        collect_diagonal); collective when the object is distributed."""
+        self._check_up()
+        from .distla import ops
+        from .distla.objects import DevObj
+        from .errors import DimensionMismatch
+        obj = self.fetch(name)
+        if not isinstance(obj, DevObj):
+            raise DimensionMismatch(f"{name!r} is not a distributed object")
+        return ops.diagonal_of(self, obj) if diagonal else ops.dense_of(self, obj)
+
     def synchronize(self):
         _torch().cuda.synchronize(self.device)
 
@@ -245,6 +267,20 @@ class B200Cluster:
             self.shutdown()
         except Exception:
             pass
+
+
+# ops whose per-rank results are gathered for run(); the others return None
+# everywhere ("distla.collect": rank 1 returns the whole object, the other
+# ranks nothing, so the reference's merge of per-rank pieces still works)
+GATHERED_OPS = ("distla.cholesky", "distla.logdet", "distla.sumsq")
+
+
+def per_rank_results(comm, fn_id, result, G):
+    if fn_id in GATHERED_OPS:
+        return comm.all_gather_object(result)
+    if fn_id == "distla.collect":
+        return [result] + [{} for _ in range(G - 1)]
+    return [result] * G
 
 
 def _copy_value(value):

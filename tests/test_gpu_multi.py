@@ -1,11 +1,14 @@
 """The G > 1 code path end to end on the GPU box.
 
-Two (or four) processes share cuda:0 and talk over gloo: every process drives
-its own share of the 2-D block-cyclic tiles with the real libbgp tile kernels
-(construct_tiles, tile_potrf, panel_trsm, the DMMA tile-list update,
-tile_trsv, tile_gemv, tile_logdet).  No kernel waits on another process (all
-exchanges are host-side gloo collectives), so sharing one GPU is safe.  On
-an 8 x B200 box the same code runs with NCCL, one GPU per process.
+Two, four or eight processes share cuda:0 and talk over gloo: every process
+drives its own share of the 2-D block-cyclic tiles (plus its shadow diagonal
+tiles) with the real libbgp kernels (construct_tiles, the one-launch sweep
+step bgp_dist_step with its in-launch POTRF / inverse / panel solve + push,
+tile_trsv, tile_gemv, tile_logdet).  No kernel waits on another process (the
+steps are ordered by host-side gloo barriers), so sharing one GPU is safe.
+On an 8 x B200 box the same code runs with NCCL, one GPU per process.
+test_master_spawn_* drive the same path through spawn(P) from this process
+(transport.master: P worker processes, per-rank results in rank order).
 """
 
 import os
@@ -59,7 +62,8 @@ def _worker(rank, world, port, q, xfer="push"):
         x = distla.triangular_solve(cl, L, u, "x", side="back")
         out["x"] = distla.collect(cl, x)
         out["logdet"] = distla.log_det_from_chol(cl, L)
-        out["owned"] = stats[0]["owned_blocks"]
+        assert len(stats) == world  # per-rank stats, gathered
+        out["owned"] = stats[rank]["owned_blocks"]
         # NotPositiveDefinite is agreed by every rank and leaves no factor
         Cn = distla.distribute(cl, "Cn", -np.eye(300), "triangular", distla.make_layout(300, cl.grid, h=1))
         try:
@@ -82,7 +86,7 @@ def _worker(rank, world, port, q, xfer="push"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,xfer", [(2, "push"), (4, "push"), (2, "nccl")])
+@pytest.mark.parametrize("world,xfer", [(2, "push"), (4, "push"), (8, "push"), (2, "nccl")])
 def test_multi_rank_path_on_one_gpu(world, xfer):
     """xfer "push": the panel TRSM stores into every rank's IPC-mapped panel
     buffer (bgp_panel_trsm_push; here all mappings are on cuda:0); "nccl":
@@ -137,3 +141,48 @@ def test_multi_rank_path_on_one_gpu(world, xfer):
         assert relerr(r["pv"], want_pv) <= 1e-9
     lls = [r["ll"] for r in res.values()]
     assert all(v == lls[0] for v in lls)  # identical on every rank
+
+
+def test_master_spawn_reference_call_sequence():
+    """The reference's call sequence unchanged at P = 2 from a plain process:
+    spawn(2) -> KrigeProblem(...).log_density() / predict, distla calls with
+    P-length per-rank results (bg/transport/base.py:213-234)."""
+    from oracle import blockgp_oracle as orc
+    from paper_1305_4886_b200 import distla, spawn
+    from paper_1305_4886_b200.errors import NotPositiveDefinite
+    from paper_1305_4886_b200.gp import KrigeProblem, builtin_spec
+    cl = spawn(2, tile=128, devices=[0, 0])
+    try:
+        assert cl.P == 2 and cl.comm_backend == "gloo"
+        n = 500
+        A = spd_matrix(n, seed=9)
+        lay = distla.make_layout(n, cl.grid, h=2)
+        C = distla.distribute(cl, "C", A, "triangular", lay)
+        L, stats = distla.distributed_cholesky(cl, C, "L")
+        assert len(stats) == 2
+        T = -(-n // 128)
+        assert sum(s["owned_blocks"] for s in stats) == T * (T + 1) // 2
+        assert relerr(distla.collect(cl, L), np.linalg.cholesky(A)) <= 1e-12
+        parts = cl.run("distla.logdet", l_name="L")
+        assert len(parts) == 2
+        assert abs(sum(parts) - np.linalg.slogdet(A)[1]) <= 1e-12 * abs(sum(parts))
+        with pytest.raises(NotPositiveDefinite) as ei:
+            Cn = distla.distribute(cl, "Cn", -np.eye(300), "triangular",
+                                   distla.make_layout(300, cl.grid, h=1))
+            distla.distributed_cholesky(cl, Cn, "Ln")
+        assert ei.value.block_index == 1 and "Ln" not in cl.remote_ls()
+        kern, X, theta, extra, z = orc.config_inputs(1, n=700)
+        y = np.linalg.cholesky(orc.dense_cov(kern, theta, X, **extra)) @ z
+        Xp = orc.c3_pred_coords(12)
+        prob = KrigeProblem(cl, "g", builtin_spec(kern, X, Xp, **extra), y, theta, m=len(Xp))
+        ll = prob.log_density()
+        mean, se = prob.predict(se_fit=True)
+        assert len(prob.last_cholesky_stats) == 2
+    finally:
+        cl.shutdown()
+    ref = orc.OracleProblem(kern, X, y, theta, pred_coords=Xp, **extra)
+    want = ref.log_density()
+    rmean, rse = ref.predict(se_fit=True)
+    assert abs(ll - want) <= 1e-10 * abs(want)
+    assert relerr(mean, rmean) <= 1e-9 and relerr(se, rse) <= 1e-9
+    assert cl.state == "shutdown"

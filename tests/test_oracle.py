@@ -124,3 +124,13 @@ def test_config4_input_recipe():
     data = np.load("tests/golden/c4_inputs.npz")
     np.testing.assert_array_equal(data["X"], X)
     np.testing.assert_array_equal(data["z"], z)
+
+
+def test_full_eval_packed_sweep_matches_reference(golden, golden_scalars):
+    """oracle/full_eval.py (the packed-block restatement timed on the GPU
+    host as the full CPU baseline) reproduces the reference's C1 ll."""
+    from oracle import full_eval
+    kern, X, theta, extra, z = orc.config_inputs(1)
+    r = full_eval.log_density(X, golden["c1_y"], theta)
+    assert r["block"] == 683
+    assert abs(r["ll"] - golden_scalars["c1"]["ll"]) <= 1e-13 * abs(r["ll"])

@@ -1,8 +1,9 @@
 """Multi-GPU schedule (paper_1305_4886_b200/parallel.py) on CPU ranks over gloo.
 
 The 2-D block-cyclic Cholesky, the distributed forward/back solves and the
-rank-ordered log-det run here with world size 2 (1x2 grid) and 4 (2x2 grid)
-on CPU processes.  The collectives are real torch.distributed calls (gloo);
+rank-ordered log-det run here with world size 2 (1x2 grid), 4 (2x2 grid) and
+8 (2x4 grid) on CPU processes, with both panel exchanges: the push (panel
+buffers in shared memory, written by the solving rank) and the broadcast.  The collectives are real torch.distributed calls (gloo);
 the tile arithmetic is a numpy/scipy stand-in (test-only), so what is
 checked is the schedule: ownership, panel broadcasts, item lists, reduction
 and solve order.  On GPUs the same functions drive libbgp over NCCL.
@@ -19,10 +20,18 @@ from conftest import relerr, spd_matrix
 
 
 class NumpyTileOps:
-    """Tile kernels in numpy on torch CPU tensors (column-major tiles)."""
+    """Tile kernels in numpy on torch CPU tensors (column-major tiles).
 
-    def __init__(self, b, n):
+    Mirrors the device semantics the schedule relies on: a sweep step is
+    the update of every listed tile, then (plan.diag) the factorization and
+    inverse of the diagonal copy and the solve of the rank's panel tiles,
+    each solved tile also copied into every rank's panel buffer (push); once
+    a pivot failed, later steps are skipped (the device status)."""
+
+    def __init__(self, b, n, xchg=None):
         self.b, self.n = b, n
+        self.xchg = xchg
+        self.info = 0
 
     def empty(self, shape):
         import torch
@@ -44,22 +53,16 @@ class NumpyTileOps:
         return 0
 
     def begin(self):
-        pass
+        self.info = 0
 
-    def end(self, info):
-        return info
+    def end(self, info=0):
+        return info or self.info
 
-    def potrf_factor(self, local, k, row0, inv):
-        info = self.potrf(local, k, row0)
-        if info == 0 and inv is not None:
-            self._m(inv)[:] = np.linalg.inv(np.tril(self._m(local[k])))
-        return info
+    def panel_exchange(self, comm, T):
+        return self.xchg
 
-    def trsm_inv(self, inv, local, start, count):
-        Li = self._m(inv)
-        for t in range(start, start + count):
-            M = self._m(local[t])
-            M[:] = M @ Li.T
+    def sweep_begin(self, T):
+        self.info = 0
 
     def prepare_items(self, per_step):
         return [np.asarray(a).reshape(-1, 4) for a in per_step]
@@ -67,30 +70,39 @@ class NumpyTileOps:
     def prepare_gemv_items(self, per_step):
         return [np.asarray(a).reshape(-1, 2) for a in per_step]
 
-    def copy_tile(self, dst, local, k):
-        dst.copy_(local[k])
-
     def copy_tiles(self, dst, local, start, count):
         dst.copy_(local[start:start + count])
 
-    def trsm(self, diag, local, start, count):
-        L = np.tril(self._m(diag))
-        for t in range(start, start + count):
+    def _factor_solve(self, local, d, row0, trsm, push):
+        info = self.potrf(local, d, row0)
+        if info:
+            self.info = self.info or info
+            return
+        s, c = trsm
+        if c == 0:
+            return
+        Li = np.linalg.inv(np.tril(self._m(local[d])))
+        for t in range(s, s + c):
             M = self._m(local[t])
-            M[:] = la.solve_triangular(L, M.T, lower=True).T
+            M[:] = M @ Li.T
+        if push is not None:
+            xchg, which, slot0 = push
+            for buf in xchg.dest[which]:
+                buf[slot0:slot0 + c].copy_(local[s:s + c])
 
-    def side(self):
-        import contextlib
-        return contextlib.nullcontext()
+    def first_panel(self, local, d, trsm, push):
+        if not self.info:
+            self._factor_solve(local, d, 0, trsm, push)
 
-    def join_side(self):
-        pass
-
-    def update(self, local, panel, items, reserve=False):
-        for c, a, b, lower in items:
+    def step(self, J, local, panel, items, plan, par, push):
+        if self.info:
+            return
+        for c, a, b, flags in items:
             M = self._m(local[c])
             U = self._m(panel[a]) @ self._m(panel[b]).T
-            M[:] -= np.tril(U) if lower else U
+            M[:] -= np.tril(U) if flags & 1 else U
+        if plan.diag >= 0:
+            self._factor_solve(local, plan.diag, plan.diag_row0, plan.trsm, push)
 
     def sub_into(self, out, a, b):
         out.copy_(a - b)
@@ -117,13 +129,39 @@ class NumpyTileOps:
         return s, 0
 
 
+class SharedPanelExchange:
+    """CPU stand-in of parallel.PanelExchange: every rank's two panel buffers
+    live in shared memory (made by the test's parent process), so a push
+    really writes into the other processes' buffers and the schedule's
+    barriers are what keeps a rank from overwriting a panel a peer still
+    reads."""
+
+    def __init__(self, all_bufs, rank):
+        # all_bufs[r][w]: rank r's buffer w, (tiles, b, b)
+        self.bufs = list(all_bufs[rank])
+        self.dest = [[all_bufs[r][w] for r in range(len(all_bufs))] for w in range(2)]
+        self.tiles = self.bufs[0].shape[0]
+
+
+def _local_tiles(td, P, b):
+    """This rank's tile stack (owned tiles, then shadow diagonal tiles) of
+    the padded dense matrix P."""
+    import torch
+    st = td.storage_tiles
+    local = torch.zeros((len(st), b, b), dtype=torch.float64)
+    for k, (I, J) in enumerate(st):
+        blk = P[I * b:(I + 1) * b, J * b:(J + 1) * b]
+        local[k].numpy().T[:] = np.tril(blk) if I == J else blk
+    return local
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, b, q):
+def _worker(rank, world, port, n, b, q, bufs):
     import torch
     import torch.distributed as dist
 
@@ -140,35 +178,55 @@ def _worker(rank, world, port, n, b, q):
         for t in range(n, T * b):
             P[t, t] = 1.0
         td = TileDist(n, b, DeviceGrid(world), rank)
-        local = torch.zeros((td.count, b, b), dtype=torch.float64)
-        for k, (I, J) in enumerate(td.tiles):
-            blk = P[I * b:(I + 1) * b, J * b:(J + 1) * b]
-            local[k].numpy().T[:] = np.tril(blk) if I == J else blk
-        ops, comm = NumpyTileOps(b, n), TorchComm()
+        local = _local_tiles(td, P, b)
+        xchg = SharedPanelExchange(bufs, rank) if bufs is not None else None
+        ops, comm = NumpyTileOps(b, n, xchg), TorchComm()
         info = dist_cholesky(td, local, ops, comm)
         # gather L into a dense matrix on every rank
         Ld = torch.zeros((T * b, T * b), dtype=torch.float64)
         for k, (I, J) in enumerate(td.tiles):
             Ld[I * b:(I + 1) * b, J * b:(J + 1) * b] = torch.from_numpy(local[k].numpy().T.copy())
         dist.all_reduce(Ld)
+        # the shadow copies of the diagonal tiles factor to the owner's L
+        shadow_ok = all(np.array_equal(np.tril(local[td.shadow_local[K]].numpy().T),
+                                       Ld.numpy()[K * b:(K + 1) * b, K * b:(K + 1) * b])
+                        for K in td.shadows)
+        ops.xchg = None
         y = torch.zeros(T * b, dtype=torch.float64)
         y[:n] = torch.from_numpy(np.random.default_rng(3).standard_normal(n))
         u, info_f = dist_trsv(td, local, y, ops, comm, forward=True)
         x, info_b = dist_trsv(td, local, u, ops, comm, forward=False)
         ld, info_l = dist_logdet(td, local, ops, comm)
         q.put((rank, info, info_f, info_b, info_l, np.tril(Ld.numpy()[:n, :n]), u.numpy()[:n].copy(),
-               x.numpy()[:n].copy(), ld, td.count))
+               x.numpy()[:n].copy(), ld, td.count, shadow_ok))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,b", [(2, 37, 8), (2, 100, 16), (4, 90, 8), (4, 37, 16)])
-def test_distributed_cholesky_solves_logdet(world, n, b):
+def _shared_bufs(world, n, b):
+    import torch
+    T = -(-n // b)
+    out = []
+    for _ in range(world):
+        pair = []
+        for _ in range(2):
+            t = torch.full((max(T, world), b, b), float("nan"), dtype=torch.float64)
+            t.share_memory_()
+            pair.append(t)
+        out.append(pair)
+    return out
+
+
+@pytest.mark.parametrize("xfer", ["push", "broadcast"])
+@pytest.mark.parametrize("world,n,b", [(2, 37, 8), (2, 100, 16), (4, 90, 8), (4, 37, 16),
+                                       (8, 100, 8), (8, 61, 4)])
+def test_distributed_cholesky_solves_logdet(world, n, b, xfer):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q)) for r in range(world)]
+    bufs = _shared_bufs(world, n, b) if xfer == "push" else None
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q, bufs)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=240) for _ in range(world)]
@@ -180,8 +238,9 @@ def test_distributed_cholesky_solves_logdet(world, n, b):
     Lref = np.linalg.cholesky(A)
     T = -(-n // b)
     assert sum(o[9] for o in out) == T * (T + 1) // 2      # tiles partitioned
-    for rank, info, info_f, info_b, info_l, L, u, x, ld, _ in out:
+    for rank, info, info_f, info_b, info_l, L, u, x, ld, _, shadow_ok in out:
         assert info == info_f == info_b == info_l == 0
+        assert shadow_ok
         assert relerr(L, Lref) <= 1e-12
         assert relerr(u, np.linalg.solve(Lref, y)) <= 1e-12
         assert relerr(x, np.linalg.solve(A, y)) <= 1e-10
@@ -193,7 +252,6 @@ def test_distributed_cholesky_solves_logdet(world, n, b):
 
 
 def _fail_worker(rank, world, port, q):
-    import torch
     import torch.distributed as dist
 
     from paper_1305_4886_b200.grid import DeviceGrid
@@ -205,28 +263,25 @@ def _fail_worker(rank, world, port, q):
         A = -np.eye(n)
         A[:8, :8] = spd_matrix(8, seed=1)     # block 0 fine, block 1 fails
         td = TileDist(n, b, DeviceGrid(world), rank)
-        local = torch.zeros((td.count, b, b), dtype=torch.float64)
-        for k, (I, J) in enumerate(td.tiles):
-            blk = A[I * b:(I + 1) * b, J * b:(J + 1) * b]
-            local[k].numpy().T[:] = np.tril(blk) if I == J else blk
-        info = dist_cholesky(td, local, NumpyTileOps(b, n), TorchComm())
+        info = dist_cholesky(td, _local_tiles(td, A, b), NumpyTileOps(b, n), TorchComm())
         q.put(info)
     finally:
         dist.destroy_process_group()
 
 
-def test_failure_is_agreed_by_all_ranks():
+@pytest.mark.parametrize("world", [2, 4])
+def test_failure_is_agreed_by_all_ranks(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_fail_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    infos = [q.get(timeout=240) for _ in range(2)]
+    infos = [q.get(timeout=240) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
-    assert infos[0] == infos[1] == 9   # first row of tile 1 (1-based)
+    assert infos == [9] * world   # first row of tile 1 (1-based)
 
 
 def test_tile_dist_layout_invariants():
@@ -246,6 +301,20 @@ def test_tile_dist_layout_invariants():
                 assert c == cnt
                 assert [int(I) for I in dists[root].tiles[s:s + c, 0]] == \
                        [I for I in range(J + 1, T) if slot[I] >= off and slot[I] < off + cnt]
+            # step plans: every rank holding panel-(J+1) tiles factors a
+            # copy of (J+1, J+1); gates cover exactly its column-(J+1) items
+            for r, d in enumerate(dists):
+                plan = d.step_plan(J, slot)
+                ps, pc_ = d.my_panel(J + 1)
+                assert plan.trsm == ((ps, pc_) if plan.diag >= 0 else (ps, 0))
+                if pc_:
+                    assert plan.diag >= 0
+                if d.owner(J + 1, J + 1) == r:
+                    assert plan.diag == d.local[(J + 1, J + 1)]
+                gates = plan.items[:, 3] >> 8
+                assert (gates[:plan.col_items] > 0).all() and (gates[plan.col_items:] == 0).all()
+                if plan.diag >= 0:
+                    assert sorted(gates[:plan.col_items] - 1) == list(range(1 + plan.trsm[1]))
 
 
 def test_col_shards_partition():
