@@ -2,15 +2,24 @@
 //
 // Replaces distla.construct (bg/distla/kernels.py:35-75), pad_block
 // (bg/distla/objects.py:60-80) and the entrywise generators of
-// bg/gp/kernels.py:16-172.  One CTA writes one b x b tile; threads own tile
-// rows (contiguous in the column-major tile), loop over tile columns, and keep
-// the row point in registers and the tile's column points in shared memory, so
-// every store is a fully coalesced 2 KB column segment.  The kernel is bound by
-// the HBM write stream (8 B per entry) plus one FP64 exp per entry.
+// bg/gp/kernels.py:16-172.  One CTA writes one b x b tile (column-major).
 //
-// Numerics follow numpy's evaluation order exactly (no FMA contraction:
-// __dmul_rn/__dadd_rn/__ddiv_rn), so entries match the reference to the ulp
-// of exp().
+// Interior tiles of the 2-D built-in kernels (all but the T diagonal /
+// padded ones) take the fast path: a thread owns two adjacent rows, keeps
+// their points in registers, reads each column point once from shared
+// memory (16-byte loads) and writes both entries of a column with one
+// 16-byte store -- a warp stores 512 contiguous bytes per column.  Per entry
+// it spends ~23 FP64 instructions: difference, squared distance (one FMA),
+// sqrt, one multiply by sqrt(2 nu)/rho, and exp by a 64-entry table of
+// sigma^2 2^(j/64) (so the variance costs nothing) with a degree-5 polynomial
+// and magic-number rounding (no FP64<->int conversions, no branch).  The
+// kernel is bound by the HBM write stream (8 B per entry) and the FP64 issue
+// rate together.
+//
+// Numerics: the generic path (diagonal / padded tiles, other generators)
+// follows numpy's evaluation order exactly (no FMA contraction); the fast
+// path's entries differ from numpy's by a few ulp (<= 1e-15 absolute for
+// entries <= sigma^2; the tests hold them to 1e-14, pkg/tests/test_distla.py:50).
 #include "bgp_common.cuh"
 #include "bgp_internal.h"
 
@@ -79,62 +88,72 @@ __device__ __forceinline__ double gen_eval(const GenDev& g, const double* xi, co
 
 constexpr int kCovThreads = 256;
 
-// Specialised correlation for the common generators in 2-D (KIND 1..3:
-// Matern nu = 1/2, 3/2, 5/2; KIND 4: squared exponential), same operation
-// order as gen_eval (numpy's), without the per-entry family / dimension
-// dispatch; KIND 0 is the generic path.
-// x / rho through the reciprocal with one residual correction: the correctly
-// rounded quotient for all but rare ties (vs __ddiv_rn's special-case path)
-__device__ __forceinline__ double div_rho(double x, double rho, double rinv) {
-  const double q = __dmul_rn(x, rinv);
-  return fma(fma(-q, rho, x), rinv, q);
-}
+// Fast path for the common generators in 2-D (KIND 1..3: Matern nu = 1/2,
+// 3/2, 5/2; KIND 4: squared exponential); KIND 0 is the generic path.
+__device__ double kExp2Tab[64];  // 2^(j/64), host-computed (init_exp_table)
 
-// exp(x) for x <= 0 by table: x log2(e) = n + j/64 + f, |f| <= 1/128, so
-// exp(x) = 2^n * 2^(j/64) * exp(r), |r| <= ln2/128, with a degree-6
-// polynomial (truncation < 1e-18): within ~1 ulp of exp, about half the
-// FP64 instructions of the library exp.  Underflow (x < -708) -> 0.
-__device__ double kExp2Tab[64];  // 2^(j/64); read through L1 (__ldg): indices diverge across a warp
-__device__ __forceinline__ double exp_neg(double x) {
-  if (x < -708.0) return 0.0;
-  const double kd = rint(x * 92.33248261689366);  // 64 / ln 2
-  const int k = (int)kd;
-  double r = fma(kd, -0.010830424696249145, x);  // Cody-Waite: ln2/64 = hi + lo
-  r = fma(kd, -3.623510646634843e-19, r);
-  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(r, p, 1.0 / 24.0);
-  p = fma(r, p, 1.0 / 6.0);
+// sigma^2 exp(x) for x <= 0: x 64/ln2 = k + f by magic-number rounding
+// (k in the low word of t), exp(x) = 2^(k>>6) 2^((k&63)/64) exp(r),
+// |r| <= ln2/128, exp(r) by a degree-5 polynomial (truncation < 4e-17); the
+// table holds sigma^2 2^(j/64).  Below 2^-1020 the result is 0 (the
+// reference's exp underflows there as well, to within 1e-307).
+// constant-bank operands of the fast path's FP64 instructions (an FP64
+// immediate must have a zero low word; these do not)
+__constant__ double kExpC[6] = {92.33248261689366, -0.010830424696249145, -3.623510646634843e-19,
+                                1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+__device__ __forceinline__ double exp_scaled(double x, const double* __restrict__ tab) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, kExpC[0], magic);  // x 64 / ln2
+  const double kd = t - magic;
+  const int k = __double2loint(t);
+  double r = fma(kd, kExpC[1], x);  // Cody-Waite: ln2/64 = hi + lo
+  r = fma(kd, kExpC[2], r);
+  double p = fma(r, kExpC[3], kExpC[4]);
+  p = fma(r, p, kExpC[5]);
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
-  const int n = k >> 6, j = k & 63;  // k <= 0: arithmetic shift floors
-  const double v = __ldg(&kExp2Tab[j]) * p;
-  return __hiloint2double(__double2hiint(v) + (n << 20), __double2loint(v));
+  const int n = k >> 6;  // k <= 0: arithmetic shift floors
+  const double v = tab[k & 63] * p;
+  const double w = __hiloint2double(__double2hiint(v) + (n << 20), __double2loint(v));
+  return n < -1020 ? 0.0 : w;
 }
 
+// sqrt(q), q >= 0, to ~1 ulp without the library's special-case branch:
+// hardware rsqrt seed, one cubic correction (y = q^-1/2 to ~2^-70), d = q y.
+// q below 2^-1022 (coincident points) gives 0.
+__device__ __forceinline__ double sqrt_fast(double q) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  const double e = fma(-q, y * y, 1.0);
+  y = fma(y * e, fma(e, 0.375, 0.5), y);
+  const double d = q * y;
+  return __double2hiint(q) < 0x00100000 ? 0.0 : d;
+}
+
+// sigma^2 * corr(d) for the fast path from the squared distance q; sc =
+// sqrt(2 nu) / rho (Matern) or 1 / rho (squared exponential)
 template <int KIND>
-__device__ __forceinline__ double corr2d(double dx, double dy, const GenDev& g, double rinv) {
-  const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-  if (KIND == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 * (d/rho)**2)
-    const double t = div_rho(dist, g.p[1], rinv);
-    return exp_neg(__dmul_rn(-0.5, __dmul_rn(t, t)));
+__device__ __forceinline__ double cov_fast(double q, double sc, const double* __restrict__ tab) {
+  if (KIND == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 (d/rho)^2) = exp(-0.5 q / rho^2)
+    return exp_scaled(-0.5 * (q * (sc * sc)), tab);
   }
-  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) * d / rho
-  const double sv = div_rho(__dmul_rn(g.sqrt2nu, dist), g.p[1], rinv);
-  const double e = exp_neg(-sv);
+  const double sv = sqrt_fast(q) * sc;  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) d / rho
+  const double e = exp_scaled(-sv, tab);
   if (KIND == 1) return e;
-  if (KIND == 2) return __dmul_rn(__dadd_rn(1.0, sv), e);
-  return __dmul_rn(__dadd_rn(__dadd_rn(1.0, sv), __ddiv_rn(__dmul_rn(sv, sv), 3.0)), e);
+  if (KIND == 2) return fma(sv, e, e);
+  return fma(fma(sv, 1.0 / 3.0, 1.0) * sv, e, e);
 }
 
 // triangular: one CTA per lower tile (flat packed index, or an explicit
 // (I, J) list for a rank's share of a 2-D block-cyclic distribution)
 template <bool kPts, int KIND>
-__global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const double* __restrict__ X,
+__global__ void __launch_bounds__(kCovThreads, 5) cov_tri_kernel(GenDev g, const double* __restrict__ X,
                                                               int64_t n, int T, int b,
                                                               double* __restrict__ out,
                                                               const int32_t* __restrict__ tile_ij) {
-  extern __shared__ double colpts[];  // b * dim
+  extern __shared__ __align__(16) double colpts[];  // b * dim
+  __shared__ double tab[64];          // fast path: sigma^2 2^(j/64)
   int I, J;
   if (tile_ij) {
     I = tile_ij[2 * blockIdx.x];
@@ -148,24 +167,46 @@ __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const do
     int64_t jj = j0 + t / dim;
     colpts[t] = (kPts && jj < n) ? X[jj * dim + t % dim] : 0.0;
   }
+  // interior tiles (no padding, off the diagonal): no per-entry checks
+  // tiles without padding (all but the last tile row) take the fast path;
+  // on diagonal tiles it masks the strict upper triangle and adds the nugget
+  const bool interior = KIND != 0 && i0 + b <= n && j0 + b <= n;
+  if (interior && threadIdx.x < 64) tab[threadIdx.x] = g.p[0] * kExp2Tab[threadIdx.x];
   __syncthreads();
   double* tile = out + (int64_t)blockIdx.x * b * b;
-  // interior tiles (no padding, off the diagonal): no per-entry checks
-  const bool interior = KIND != 0 && I != J && i0 + b <= n && j0 + b <= n;
+  if (interior) {
+    // thread -> row pair (t mod b/2) over a contiguous share of the columns
+    const int npairs = b / 2, nsplit = blockDim.x / npairs;
+    const int pr = threadIdx.x % npairs, part = threadIdx.x / npairs;
+    if (part >= nsplit) return;
+    const int r = 2 * pr, cw = b / nsplit, c0 = part * cw;
+    const double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r));
+    const double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r + 1));
+    const double sc = KIND == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
+    const double tau2 = (g.nugget && g.part == BGP_PART_COV) ? g.p[g.np - 1] : 0.0;
+    const double2* cp = reinterpret_cast<const double2*>(colpts);
+    double2* dst = reinterpret_cast<double2*>(tile + r);
+#pragma unroll 4
+    for (int c = c0; c < c0 + cw; ++c) {
+      const double2 pc = cp[c];
+      const double ax = x0.x - pc.x, ay = x0.y - pc.y;
+      const double bx = x1.x - pc.x, by = x1.y - pc.y;
+      double2 v;
+      v.x = cov_fast<KIND>(fma(ax, ax, ay * ay), sc, tab);
+      v.y = cov_fast<KIND>(fma(bx, bx, by * by), sc, tab);
+      if (I == J) {  // rows r, r+1 of a diagonal tile: lower part, nugget where i == j
+        v.x = c > r ? 0.0 : (c == r ? v.x + tau2 : v.x);
+        v.y = c > r + 1 ? 0.0 : (c == r + 1 ? v.y + tau2 : v.y);
+      }
+      __stcs(dst + (int64_t)c * (b / 2), v);
+    }
+    return;
+  }
   for (int r = threadIdx.x; r < b; r += blockDim.x) {
     const int64_t i = i0 + r;
     double xi[kMaxDim];
 #pragma unroll
     for (int d = 0; d < kMaxDim; ++d) xi[d] = (kPts && d < dim && i < n) ? X[i * dim + d] : 0.0;
-    if (interior) {
-      const double p0 = g.p[0], rinv = 1.0 / g.p[1];
-#pragma unroll 4
-      for (int c = 0; c < b; ++c) {
-        const double dx = xi[0] - colpts[2 * c], dy = xi[1] - colpts[2 * c + 1];
-        tile[(int64_t)c * b + r] = __dmul_rn(p0, corr2d<KIND>(dx, dy, g, rinv));
-      }
-      continue;
-    }
     const int cmax = (I == J) ? r : b - 1;
     for (int c = 0; c < b; ++c) {
       const int64_t j = j0 + c;
@@ -226,7 +267,7 @@ __global__ void cov_vec_kernel(GenDev g, int64_t n, int64_t padded, double* __re
   }
 }
 
-// specialised kernel variant for a generator (see corr2d)
+// fast-path variant for a generator (see cov_fast)
 static int cov_kind(const GenDev& g) {
   if (g.dim != 2 || (g.part != BGP_PART_COV && g.part != BGP_PART_CROSS && g.part != BGP_PART_PRED)) return 0;
   if (g.family == BGP_GEN_MATERN && g.nucode >= 0 && g.nucode <= 2) return 1 + g.nucode;

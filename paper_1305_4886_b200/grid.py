@@ -99,6 +99,22 @@ def grid_from_process_count(P):
     return ProcessGrid(triangular_order(P))
 
 
+def block_owner(I, J, grid):
+    """Reference-layout owner coordinate of lower block (I, J): both indices
+    folded to their residue in 1..D and sorted (bg/grid.py:116-139).  Kept so
+    layout queries of reference code resolve; the device uses DeviceGrid."""
+    if J > I:
+        raise OutOfTriangle(f"block ({I},{J}) above the diagonal")
+    a, c = (I - 1) % grid.D + 1, (J - 1) % grid.D + 1
+    return (max(a, c), min(a, c))
+
+
+def triangular_blocks(coord, layout, grid):
+    """Reference-layout lower blocks held by worker `coord`, column-major."""
+    return [(I, J) for J in range(1, layout.B + 1) for I in range(J, layout.B + 1)
+            if block_owner(I, J, grid) == tuple(coord)]
+
+
 def _grid_shape(G):
     """Pr x Pc with Pr <= Pc, Pr*Pc = G, as square as possible (1x1, 1x2, 2x2, 2x4)."""
     pr = isqrt(G)

@@ -58,10 +58,30 @@ def checksum(X):
             "first": [float(v) for v in X.ravel()[:4]]}
 
 
+def blocked_cholesky(A, bs=4096):
+    """In-place right-looking block Cholesky of the lower triangle (LAPACK on
+    the diagonal blocks, BLAS-3 updates): one dpotrf call on a 32,768-point
+    covariance crashes inside OpenBLAS here."""
+    import scipy.linalg as la
+    n = len(A)
+    for j0 in range(0, n, bs):
+        j1 = min(n, j0 + bs)
+        Ljj = la.cholesky(A[j0:j1, j0:j1], lower=True, check_finite=False)
+        A[j0:j1, j0:j1] = Ljj
+        if j1 < n:
+            P = la.solve_triangular(Ljj, A[j1:, j0:j1].T, lower=True, check_finite=False).T
+            A[j1:, j0:j1] = P
+            for c0 in range(j1, n, bs):
+                c1 = min(n, c0 + bs)
+                A[c0:, c0:c1] -= P[c0 - j1:] @ P[c0 - j1:c1 - j1].T
+    return np.tril(A)
+
+
 def simulate(kern, X, theta, extra, z):
     C = dense_cov(kern, theta, X, **extra)
-    y = np.linalg.cholesky(C) @ z
-    del C
+    L = np.linalg.cholesky(C) if len(X) <= 16384 else blocked_cholesky(C)
+    y = L @ z
+    del C, L
     return y
 
 

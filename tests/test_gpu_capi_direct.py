@@ -86,3 +86,37 @@ def test_bad_arguments_are_rejected(abi):
     info = ctypes.c_int64(0)
     t = torch.zeros((1, 128, 128), dtype=torch.float64, device="cuda")
     assert lib.bgp_potrf(ctx, _p(t), 100, 100, ctypes.byref(info), s) != 0  # tile not a multiple of 128
+
+
+def test_gemm_launches_on_two_streams_do_not_share_counters(abi):
+    """A trailing update and a panel solve enqueued on two streams with no
+    host synchronisation between them (they overlap on the GPU): each launch
+    owns its task counter (a ring slot zeroed on its own stream), so neither
+    re-runs nor steals the other's tasks.  Both results against numpy."""
+    lib, ctx, s, torch = abi
+    b, nt = 256, 60
+    rng = np.random.default_rng(4)
+    mats = lambda k: torch.from_numpy(rng.standard_normal((k, b, b))).cuda()  # noqa: E731
+    C, A, B = mats(nt), mats(nt), mats(nt)
+    C0 = C.clone()
+    items = torch.tensor([[k, k, (k + 1) % nt, 0] for k in range(nt)], dtype=torch.int32).cuda()
+    L = np.linalg.cholesky(spd_matrix(b, seed=1))
+    Linv = torch.from_numpy(np.ascontiguousarray(np.linalg.inv(L).T)).cuda()  # column-major tile
+    X = mats(40)
+    X0 = X.clone()
+    s2 = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        assert lib.bgp_tile_update(ctx, _p(C), _p(A), _p(B), _p(items), nt, b, s) == 0
+        assert lib.bgp_panel_trsm_inv(ctx, _p(Linv), _p(X), 40, b, s2.cuda_stream) == 0
+        assert lib.bgp_panel_trsm_inv(ctx, _p(Linv), _p(X), 40, b, s2.cuda_stream) == 0
+    torch.cuda.synchronize()
+    m = lambda t: t.cpu().numpy().transpose(0, 2, 1)  # noqa: E731  column-major tiles -> matrices
+    a, bb, c0 = m(A), m(B), m(C0)
+    want = np.stack([c0[k] - 3 * a[k] @ bb[(k + 1) % nt].T for k in range(nt)])
+    assert relerr(m(C), want) <= 1e-12
+    Li = np.linalg.inv(L)
+    xw = m(X0)
+    for _ in range(6):
+        xw = xw @ Li.T
+    assert relerr(m(X), xw) <= 1e-11

@@ -186,3 +186,62 @@ def test_master_spawn_reference_call_sequence():
     assert abs(ll - want) <= 1e-10 * abs(want)
     assert relerr(mean, rmean) <= 1e-9 and relerr(se, rse) <= 1e-9
     assert cl.state == "shutdown"
+
+
+class _OwnExchange:
+    """A panel exchange whose only destination is this process's buffers."""
+
+    def __init__(self, cl, tiles):
+        import ctypes
+
+        import torch
+        self.tiles = tiles
+        self.bufs = [torch.zeros((tiles, cl.tile, cl.tile), dtype=torch.float64, device=cl.device)
+                     for _ in range(2)]
+        self.dst = [(ctypes.c_void_p * 1)(t.data_ptr()) for t in self.bufs]
+
+
+class _OneRank:
+    world = 1
+
+    def barrier_stream(self):
+        pass
+
+    def broadcast(self, t, src):
+        pass
+
+    def min_nonzero(self, v):
+        return int(v)
+
+
+@pytest.mark.parametrize("tile,nt", [(128, 11), (256, 5), (512, 3)])
+@pytest.mark.parametrize("push", [True, False])
+def test_dist_sweep_steps_in_one_process(cluster_factory, tile, nt, push):
+    """The sweep-step launch (bgp_dist_step: update + in-launch POTRF /
+    inverse / gated TRSM, with or without the push epilogue) driven by
+    dist_cholesky on a 1 x 1 grid, against LAPACK."""
+    import torch
+
+    from paper_1305_4886_b200.grid import DeviceGrid
+    from paper_1305_4886_b200.parallel import LibTileOps, TileDist, dist_cholesky
+    cl = cluster_factory(tile=tile)
+    n = nt * tile - 19
+    A = spd_matrix(n, seed=tile)
+    td = TileDist(n, tile, DeviceGrid(1), 0)
+    T = td.T
+    P = np.eye(T * tile)
+    P[:n, :n] = A
+    local = torch.empty((td.storage_count, tile, tile), dtype=torch.float64, device=cl.device)
+    for k, (I, J) in enumerate(td.storage_tiles):
+        blk = P[I * tile:(I + 1) * tile, J * tile:(J + 1) * tile]
+        local[k] = torch.from_numpy(np.ascontiguousarray((np.tril(blk) if I == J else blk).T))
+    ops = LibTileOps(cl, n)
+    xchg = _OwnExchange(cl, T) if push else None
+    ops.panel_exchange = lambda comm, T: xchg
+    launches = cl.launches()
+    assert dist_cholesky(td, local, ops, _OneRank()) == 0
+    assert cl.launches() - launches <= T + 2  # one launch per step (+ the first panel)
+    L = np.zeros((T * tile, T * tile))
+    for k, (I, J) in enumerate(td.tiles):
+        L[I * tile:(I + 1) * tile, J * tile:(J + 1) * tile] = local[k].cpu().numpy().T
+    assert relerr(L[:n, :n], np.linalg.cholesky(A)) <= 1e-12

@@ -8,11 +8,12 @@ fixture that tests/golden/make_golden.py obtained by running the reference
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
 
-from conftest import relerr
+from conftest import GOLDEN, relerr
 from oracle import blockgp_oracle as orc
 
 
@@ -134,3 +135,24 @@ def test_full_eval_packed_sweep_matches_reference(golden, golden_scalars):
     r = full_eval.log_density(X, golden["c1_y"], theta)
     assert r["block"] == 683
     assert abs(r["ll"] - golden_scalars["c1"]["ll"]) <= 1e-13 * abs(r["ll"])
+
+
+def test_full_size_reference_fixtures_agree_with_survey():
+    """The full-size fixtures (make_full_configs.py, produced by the
+    reference) reproduce BASELINE.md 3's survey goldens: C2's ten ll to the
+    survey's 12 significant digits, C3's ll and ||mean||, ||se||, and the
+    coordinates regenerate from the seed."""
+    import json
+    meta = json.load(open(os.path.join(GOLDEN, "full_configs.json")))
+    c2 = [-7686.62544235, -4553.77461647, -4574.36131115, -5658.81011183, -7290.93691243,
+          -9256.45042656, -11437.3571029, -13759.4716896, -16173.2526993, -18644.7801649]
+    for got, want in zip(meta["c2"]["ll"], c2):
+        assert abs(got - want) <= 5e-12 * abs(want)
+    c3 = meta["c3"]
+    assert abs(c3["ll"] - (-1206.4571584386722)) <= 1e-10 * 1206.46
+    assert c3["norm_mean"] == pytest.approx(61.725485129258466, rel=1e-12)
+    assert c3["norm_se"] == pytest.approx(12.093826573490732, rel=1e-12)
+    for cfg, n in ((2, None), (3, None), (5, 16384), (4, None)):
+        X = orc.config_inputs(cfg, n=n)[1]
+        key = {2: "c2", 3: "c3", 5: "c5s", 4: "c4_lead"}[cfg]
+        assert float(np.sum(X)) == meta[key]["X"]["sum"]

@@ -93,15 +93,26 @@ def c2(cl, tile):
     y = simulate_y(cl, spec, theta, n, z)
     prob = KrigeProblem(cl, "c2", spec, y, theta)
     prob.log_density(np.array([2.0, 0.021, 0.05]))  # warm-up at another theta
+    lib, ctx = cl.lib, cl._ctx
+    lib.bgp_set_profiling(ctx, 1)
+    prof = (ctypes.c_double * 10)()
+    lib.bgp_profile_read(ctx, prof)  # clear
     lls, ts = [], []
     for rho in np.linspace(0.02, 0.2, 10):
         ll, t = timed(lambda: prob.log_density(np.array([2.0, rho, 0.05])))
         lls.append(ll)
         ts.append(t)
+    lib.bgp_profile_read(ctx, prof)
+    steps = (ctypes.c_double * 4096)()
+    ns = lib.bgp_profile_steps(ctx, steps, 4096)
+    lib.bgp_set_profiling(ctx, 0)
     errs = [rel(a, b) for a, b in zip(lls, SURVEY["c2_ll"])]
+    facts = max(prof[7], 1)
     return {"config": 2, "n": n, "evals_per_s": 10 / sum(ts), "total_s": sum(ts), "ll": lls,
             "max_rel_err_vs_survey_12sf": max(errs), "tol": "12 significant digits (5e-12)",
-            "tile": tile}
+            "tile": tile, "eval_ms": [1e3 * t for t in ts],
+            "cholesky_ms_per_eval": prof[8] / facts, "update_launch_ms_per_eval": prof[2] / facts,
+            "last_factorization_step_ms": [round(steps[i], 4) for i in range(ns)]}
 
 
 def c3(cl, tile):
