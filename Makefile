@@ -17,7 +17,19 @@ build/%.o: $(SRC_DIR)/%.cu $(HDRS)
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
+# checked build: device-side bounds / invariant checks (BGP_CHECK) on;
+# use with BGP_LIB_PATH=build/checked/libbgp.so (tools/sanitize_small.py)
+CHECKED_OBJS := $(patsubst $(SRC_DIR)/%.cu,build/checked/%.o,$(SRCS))
+checked: build/checked/libbgp.so
+
+build/checked/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build/checked
+	$(NVCC) $(NVFLAGS) -DBGP_CHECKED -c $< -o $@ 2> build/checked/$*.ptxas.log || (cat build/checked/$*.ptxas.log; exit 1)
+
+build/checked/libbgp.so: $(CHECKED_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHECKED_OBJS)
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean checked

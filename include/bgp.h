@@ -81,6 +81,8 @@ typedef struct {
   double params[8];    /* theta as in bg/gp/kernels.py:109-111, 174-180       */
   double nu;           /* Matern smoothness 0.5 / 1.5 / 2.5 (nu1 for product)  */
   double nu2;          /* second-axis smoothness (product kernel)             */
+  double span;         /* upper bound on any point distance (0: unknown); lets
+                          the covariance kernel skip its exp underflow test  */
 } bgp_generator;
 
 /* ---- context ------------------------------------------------------------ */
@@ -132,6 +134,21 @@ int bgp_set_tail(bgp_ctx_t ctx, int tiles);
  * transposed rectangular object B^T (m x n tiles), in place.
  * info = 0, or the 1-based global row of the first zero diagonal entry
  * (SingularDiagonal, kernels.py:245-246, 302-303). */
+/* Stream-ordered forms for pipelined evaluations (several factorizations in
+ * flight, each on its own context and stream): no host synchronization.
+ * bgp_potrf_async resets the context status and factors (a failing pivot
+ * row stays in the status; later launches of the context skip);
+ * bgp_trsv_async solves (a zero pivot goes to the status);
+ * bgp_logdet_async / bgp_sumsq_async write their scalar to device memory;
+ * bgp_info_copy copies the status (int64) to device memory. */
+int bgp_potrf_async(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, void* stream);
+int bgp_trsv_async(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x,
+                   int trans, void* stream);
+int bgp_logdet_async(bgp_ctx_t ctx, const double* L, int64_t n, int tile,
+                     double* dev_out, void* stream);
+int bgp_sumsq_async(bgp_ctx_t ctx, const double* x, int64_t n, double* dev_out,
+                    void* stream);
+int bgp_info_copy(bgp_ctx_t ctx, int64_t* dev_out, void* stream);
 int bgp_trsv(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x,
              int trans, int64_t* info, void* stream);
 int bgp_trsm_rect(bgp_ctx_t ctx, const double* L, int64_t n, int tile,

@@ -30,7 +30,7 @@ class Generator(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int), ("part", ctypes.c_int),
                 ("nugget", ctypes.c_int), ("nparams", ctypes.c_int),
                 ("params", ctypes.c_double * 8), ("nu", ctypes.c_double),
-                ("nu2", ctypes.c_double)]
+                ("nu2", ctypes.c_double), ("span", ctypes.c_double)]
 
 
 _c_dp = ctypes.c_void_p           # device pointers travel as integers
@@ -79,6 +79,11 @@ SIGNATURES = {
                                    _int, _i64, _i64, _c_dp]),
     "bgp_panel_trsm": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _i64, _int, _c_dp]),
     "bgp_tile_update": (_int, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _int, _c_dp]),
+    "bgp_potrf_async": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp]),
+    "bgp_trsv_async": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _int, _c_dp]),
+    "bgp_logdet_async": (_int, [ctypes.c_void_p, _c_dp, _i64, _int, _c_dp, _c_dp]),
+    "bgp_sumsq_async": (_int, [ctypes.c_void_p, _c_dp, _i64, _c_dp, _c_dp]),
+    "bgp_info_copy": (_int, [ctypes.c_void_p, _c_dp, _c_dp]),
     "bgp_dist_begin": (_int, [ctypes.c_void_p, _int, _int, _c_dp]),
     "bgp_dist_step": (_int, [ctypes.c_void_p, _int, _c_dp, _i64, _c_dp, _i64, _c_dp, _i64, _i64, _c_dp, _i64,
                              _i64, _i64, _int, ctypes.POINTER(ctypes.c_void_p), _int, _i64, _i64, _int, _c_dp]),

@@ -12,6 +12,26 @@ namespace bgp {
 
 // ---------------------------------------------------------------------------
 // packed lower-triangular tile index (0-based), column-major over the tile grid
+// BGP_CHECK(cond): a device-side bounds / invariant check compiled into the
+// checked build only (make checked -> build/checked/libbgp.so, -DBGP_CHECKED);
+// a failing check traps, so the launch fails and the host reports an error.
+// (compute-sanitizer is not available on this pool; tools/sanitize_small.py
+// runs the dataflow paths under the checked build instead.)
+#ifdef BGP_CHECKED
+#define BGP_CHECK(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("BGP_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define BGP_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 __host__ __device__ __forceinline__ int64_t tri_index(int64_t I, int64_t J, int64_t T) {
   return J * T - (J * (J - 1)) / 2 + (I - J);
 }

@@ -18,6 +18,7 @@ struct GenDev {
   double sqrt2nu, sqrt2nu2;
   int nucode, nucode2;  // 0: nu=1/2, 1: 3/2, 2: 5/2
   int dim;
+  int safe_exp;  // fast covariance path: no exp argument can underflow (span known)
 };
 
 struct Ctx {
@@ -182,6 +183,9 @@ struct GemmProblem {
   // zeroed int: the first CTA to take a ticket is the look-ahead CTA
   // (null: launch_gemm provides one)
   int* role_ticket;
+  // tile counts behind the A / B / C tensor maps (set by launch_gemm; the
+  // checked build asserts every tile index against them)
+  int64_t nA, nB, nC;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

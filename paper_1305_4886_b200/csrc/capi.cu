@@ -98,6 +98,13 @@ static int to_gendev(Ctx* ctx, const bgp_generator* g, int dim, GenDev* out) {
   d.sqrt2nu = std::sqrt(2.0 * g->nu);
   d.sqrt2nu2 = std::sqrt(2.0 * g->nu2);
   d.dim = dim;
+  // the largest exp argument the fast covariance path can see, from the
+  // caller's bound on point distances: below ~700 no underflow test is needed
+  if (g->span > 0.0 && g->nparams >= 2 && g->params[1] > 0.0) {
+    const double r = g->span / g->params[1];
+    const double amax = g->family == BGP_GEN_SQEXP ? 0.5 * r * r : d.sqrt2nu * r;
+    d.safe_exp = amax < 700.0;
+  }
   if ((g->family == BGP_GEN_MATERN || g->family == BGP_GEN_PRODUCT) && g->part != BGP_PART_PREDVAR &&
       d.nucode < 0) {
     ctx->err = "unsupported Matern smoothness";
@@ -479,6 +486,53 @@ int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, int64_t* info, 
     ctx->nsteps = nsteps < 4096 ? nsteps : 4096;
   }
   return rc;
+}
+
+// ---- stream-ordered log-density steps (pipelined evaluations) ----------------
+// No host synchronization: the status stays in the context (bgp_info_copy
+// moves it to caller device memory), scalars land in caller device memory.
+int bgp_potrf_async(bgp_ctx_t ctx, double* tiles, int64_t n, int tile, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_info(ctx, s);
+  if (rc) return rc;
+  gemm_prepare();
+  potrf_prepare();
+  Marks mk{ctx};
+  mk.ev = ctx->events_cap;  // no profiling marks
+  int m_start, m_p0, m_t0, J0, m_tail_end = -1;
+  return potrf_level(ctx, tiles, n, tile, s, 0, 0, mk, nullptr, &m_start, &m_p0, &m_t0, &J0, &m_tail_end);
+}
+
+int bgp_trsv_async(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* x, int trans, void* stream) {
+  if (!valid_tile(tile) || n < 1) return BGP_E_ARG;
+  return launch_trsv(ctx, L, n, tile, x, trans, (cudaStream_t)stream);
+}
+
+static int copy_red(Ctx* ctx, double* dev_out, cudaStream_t s, const char* what) {
+  cudaError_t e = cudaMemcpyAsync(dev_out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToDevice, s);
+  return e == cudaSuccess ? BGP_OK : set_err(ctx, what, e);
+}
+
+int bgp_logdet_async(bgp_ctx_t ctx, const double* L, int64_t n, int tile, double* dev_out, void* stream) {
+  if (!valid_tile(tile) || n < 1 || !dev_out) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_logdet(ctx, L, n, tile, s);
+  return rc ? rc : copy_red(ctx, dev_out, s, "logdet copy");
+}
+
+int bgp_sumsq_async(bgp_ctx_t ctx, const double* x, int64_t n, double* dev_out, void* stream) {
+  if (n < 0 || !dev_out) return BGP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_sumsq(ctx, x, n, s);
+  return rc ? rc : copy_red(ctx, dev_out, s, "sumsq copy");
+}
+
+int bgp_info_copy(bgp_ctx_t ctx, int64_t* dev_out, void* stream) {
+  if (!dev_out) return BGP_E_ARG;
+  cudaError_t e = cudaMemcpyAsync(dev_out, ctx->d_info, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? BGP_OK : set_err(ctx, "status copy", e);
 }
 
 int bgp_set_tail(bgp_ctx_t ctx, int tiles) {

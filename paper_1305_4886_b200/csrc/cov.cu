@@ -28,6 +28,10 @@
 namespace bgp {
 
 constexpr int kMaxDim = 4;
+#ifndef COV_UNROLL
+#define COV_UNROLL 8
+#endif
+constexpr int kCovUnroll = COV_UNROLL;  // columns per unrolled iteration of the fast path (2 entries each)
 
 __device__ __forceinline__ double matern_corr(double d, double rho, double sqrt2nu, int nucode) {
   // bg/gp/kernels.py:16-29: s = sqrt(2 nu) * d / rho
@@ -101,6 +105,7 @@ __device__ double kExp2Tab[64];  // 2^(j/64), host-computed (init_exp_table)
 // immediate must have a zero low word; these do not)
 __constant__ double kExpC[6] = {92.33248261689366, -0.010830424696249145, -3.623510646634843e-19,
                                 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+template <bool SAFE>
 __device__ __forceinline__ double exp_scaled(double x, const double* __restrict__ tab) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
   const double t = fma(x, kExpC[0], magic);  // x 64 / ln2
@@ -116,39 +121,45 @@ __device__ __forceinline__ double exp_scaled(double x, const double* __restrict_
   const int n = k >> 6;  // k <= 0: arithmetic shift floors
   const double v = tab[k & 63] * p;
   const double w = __hiloint2double(__double2hiint(v) + (n << 20), __double2loint(v));
-  return n < -1020 ? 0.0 : w;
+  return (SAFE || n >= -1020) ? w : 0.0;  // SAFE: the host's distance bound rules underflow out
 }
 
 // sqrt(q), q >= 0, to ~1 ulp without the library's special-case branch:
 // hardware rsqrt seed, one cubic correction (y = q^-1/2 to ~2^-70), d = q y.
-// q below 2^-1022 (coincident points) gives 0.
+// q below 2^-1022 (coincident points) is raised to 2^-1022 by one integer
+// max on its high word: d = 2^-511, which every kernel maps to corr = 1, as
+// for d = 0.
 __device__ __forceinline__ double sqrt_fast(double q) {
+  q = __hiloint2double(max(__double2hiint(q), 0x00100000), __double2loint(q));
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
   const double e = fma(-q, y * y, 1.0);
   y = fma(y * e, fma(e, 0.375, 0.5), y);
-  const double d = q * y;
-  return __double2hiint(q) < 0x00100000 ? 0.0 : d;
+  return q * y;
 }
 
 // sigma^2 * corr(d) for the fast path from the squared distance q; sc =
-// sqrt(2 nu) / rho (Matern) or 1 / rho (squared exponential)
+// sqrt(2 nu) / rho (Matern) or 1 / rho (squared exponential).  KIND & 7:
+// 1..3 Matern nu = 1/2, 3/2, 5/2, 4 squared exponential; KIND & 8: no
+// underflow test (GenDev.safe_exp)
 template <int KIND>
 __device__ __forceinline__ double cov_fast(double q, double sc, const double* __restrict__ tab) {
-  if (KIND == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 (d/rho)^2) = exp(-0.5 q / rho^2)
-    return exp_scaled(-0.5 * (q * (sc * sc)), tab);
+  constexpr int K = KIND & 7;
+  constexpr bool SAFE = (KIND & 8) != 0;
+  if (K == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 (d/rho)^2) = exp(-0.5 q / rho^2)
+    return exp_scaled<SAFE>(-0.5 * (q * (sc * sc)), tab);
   }
   const double sv = sqrt_fast(q) * sc;  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) d / rho
-  const double e = exp_scaled(-sv, tab);
-  if (KIND == 1) return e;
-  if (KIND == 2) return fma(sv, e, e);
+  const double e = exp_scaled<SAFE>(-sv, tab);
+  if (K == 1) return e;
+  if (K == 2) return fma(sv, e, e);
   return fma(fma(sv, 1.0 / 3.0, 1.0) * sv, e, e);
 }
 
 // triangular: one CTA per lower tile (flat packed index, or an explicit
 // (I, J) list for a rank's share of a 2-D block-cyclic distribution)
 template <bool kPts, int KIND>
-__global__ void __launch_bounds__(kCovThreads, 5) cov_tri_kernel(GenDev g, const double* __restrict__ X,
+__global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const double* __restrict__ X,
                                                               int64_t n, int T, int b,
                                                               double* __restrict__ out,
                                                               const int32_t* __restrict__ tile_ij) {
@@ -161,6 +172,7 @@ __global__ void __launch_bounds__(kCovThreads, 5) cov_tri_kernel(GenDev g, const
   } else {
     tri_decode(blockIdx.x, T, I, J);
   }
+  BGP_CHECK(J >= 0 && J <= I && I < T && 2 * b >= blockDim.x);
   const int dim = g.dim;
   const int64_t j0 = (int64_t)J * b, i0 = (int64_t)I * b;
   for (int t = threadIdx.x; t < b * dim; t += blockDim.x) {
@@ -182,11 +194,11 @@ __global__ void __launch_bounds__(kCovThreads, 5) cov_tri_kernel(GenDev g, const
     const int r = 2 * pr, cw = b / nsplit, c0 = part * cw;
     const double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r));
     const double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r + 1));
-    const double sc = KIND == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
+    const double sc = (KIND & 7) == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
     const double tau2 = (g.nugget && g.part == BGP_PART_COV) ? g.p[g.np - 1] : 0.0;
     const double2* cp = reinterpret_cast<const double2*>(colpts);
     double2* dst = reinterpret_cast<double2*>(tile + r);
-#pragma unroll 4
+#pragma unroll kCovUnroll
     for (int c = c0; c < c0 + cw; ++c) {
       const double2 pc = cp[c];
       const double ax = x0.x - pc.x, ay = x0.y - pc.y;
@@ -288,11 +300,13 @@ template <bool kPts>
 static void launch_cov_tri(const GenDev& g, unsigned grid, size_t smem, cudaStream_t s, const double* X, int64_t n,
                            int T, int b, double* out, const int32_t* tile_ij) {
   init_exp_table();
-  switch (kPts ? cov_kind(g) : 0) {
-    case 1: cov_tri_kernel<kPts, 1><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
-    case 2: cov_tri_kernel<kPts, 2><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
-    case 3: cov_tri_kernel<kPts, 3><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
-    case 4: cov_tri_kernel<kPts, 4><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+  const int kind = kPts ? cov_kind(g) : 0;
+  switch (kind ? kind + (g.safe_exp ? 8 : 0) : 0) {
+#define BGP_COV_CASE(K) \
+  case K: cov_tri_kernel<kPts, K><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
+    BGP_COV_CASE(1) BGP_COV_CASE(2) BGP_COV_CASE(3) BGP_COV_CASE(4)
+    BGP_COV_CASE(9) BGP_COV_CASE(10) BGP_COV_CASE(11) BGP_COV_CASE(12)
+#undef BGP_COV_CASE
     default: cov_tri_kernel<kPts, 0><<<grid, kCovThreads, smem, s>>>(g, X, n, T, b, out, tile_ij); break;
   }
 }

@@ -431,6 +431,10 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
         const int at = (int)(it.aTile0 + kt * it.aStride);
         const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, p.T)
                                        : (int)(it.bTile0 + kt * it.bStride);
+        BGP_CHECK(at >= 0 && at < (ta == tmT ? p.nC : p.nA));
+        BGP_CHECK(bt >= 0 && bt < (it.bLinv ? 1 : p.nB));
+        BGP_CHECK(it.mrow0 >= 0 && it.mrow0 + BM <= p.b && it.nrow0 >= 0 && it.nrow0 + BN <= p.b);
+        BGP_CHECK(kin + BK <= p.b);
         uint8_t* sa = gs.stages + stage * STAGE_BYTES;
         uint8_t* sb = sa + STAGE_A_BYTES;
 #pragma unroll
@@ -708,6 +712,8 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
       __syncwarp();
       if (lane == 0) {
         const int r0 = it.mrow0 + wm * WM + r * EPI_ROWS, c0 = it.nrow0 + wn * WN;
+        BGP_CHECK(it.cTile >= 0 && it.cTile < p.nC);
+        BGP_CHECK(p.npush == 0 || !it.store || (it.cTile - p.panel0 >= 0 && it.cTile - p.panel0 < p.push_tiles));
 #pragma unroll
         for (int b2 = 0; b2 < EPI_BOXES; ++b2) {
           if (it.store) {
@@ -733,6 +739,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         tma_store_wait_all0();
         fence_proxy_async_global();
         __threadfence();
+        BGP_CHECK(it.gate < (p.mode == GEMM_LIST ? p.trsm_count + 1 : (p.mode == GEMM_RECT_TRAIL ? p.Tm : p.T)));
         atomicAdd(p.col_gate + it.gate, 1);
       }
       __syncwarp();
@@ -837,6 +844,9 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   if (p_in.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
   GemmProblem p = p_in;
   p.cbase = Cbase;
+  p.nA = nA;
+  p.nB = nB;
+  p.nC = nC;
   const int64_t tasks = gemm_num_tasks(p);
   if (tasks <= 0) return BGP_OK;
   int rc;

@@ -200,6 +200,8 @@ def construct(ctx, name, kind, generator, params, inputs_name, row_layout, col_l
             Y = ctx.device_input(inputs_name, "pred_coords")
             if Y.shape[1] != dim or Y.shape[0] < m:
                 raise GeneratorError(ctx.rank, IndexError("pred_coords do not conform"))
+        keys = ("coords", "pred_coords") if g.part == _lib.PART_CROSS else (key_x,)
+        desc.span = ctx.input_span(inputs_name, keys)
     if name in ctx.store:
         del ctx.store[name]
     if kind == "triangular" and ctx.G > 1:
@@ -292,6 +294,69 @@ def cholesky(ctx, name, out_name):
         return {"peak_blocks": obj.dist.storage_count, "owned_blocks": obj.dist.count, "tile": obj.tile}
     nt = obj.data.shape[0]
     return {"peak_blocks": nt, "owned_blocks": nt, "tile": obj.tile}
+
+
+@registry.register("distla.loglik_many")
+def loglik_many(ctx, thetas, cov_fn, mean_fn, inputs_name, y_name, row_layout, lanes=2):
+    """logdet, sumsq and status of log_density at every theta of a list
+    (one GPU), pipelined: evaluation k runs on lane k mod `lanes` (its own
+    library context and stream), so the covariance build and first panels of
+    evaluation k+1 fill the SMs the latency-bound tail of evaluation k's
+    Cholesky leaves idle.  Each evaluation is the path of
+    bg/gp/problem.py:119-142 (construct, Cholesky, y - mu, forward solve,
+    logdet, sumsq) with the stream-ordered entry points; one host
+    synchronization at the end.  Returns [(logdet, ssq, info)] in order."""
+    import torch
+    if ctx.G > 1:
+        raise DimensionMismatch("loglik_many runs on one GPU (use log_density per theta)")
+    inputs = ctx.fetch(inputs_name)
+    y = _need(ctx, y_name, "vector")
+    n, b = row_layout.n, ctx.tile
+    T = _ntiles(n, b)
+    gens = []
+    for th in thetas:
+        g, desc = _device_generator(ctx, cov_fn, th, inputs, "triangular")
+        _, mdesc = _device_generator(ctx, mean_fn, th, inputs, "vector")
+        gens.append((g, desc, mdesc))
+    X = None
+    dim = 1
+    if gens and gens[0][0].family in (_lib.GEN_MATERN, _lib.GEN_SQEXP, _lib.GEN_PRODUCT):
+        X = ctx.device_input(inputs_name, "coords")
+        dim = X.shape[1]
+        span = ctx.input_span(inputs_name, ("coords",))
+        for _, desc, _ in gens:
+            desc.span = span
+    lanes = ctx.lanes(max(1, int(lanes)))
+    key = (n, b, len(lanes))
+    bufs = ctx.__dict__.get("_many_bufs")
+    if bufs is None or bufs[0] != key:
+        bufs = (key, [(ctx.empty((T * (T + 1) // 2, b, b)), ctx.empty((T * b,)), ctx.empty((T * b,)))
+                      for _ in lanes])
+        ctx.__dict__["_many_bufs"] = bufs
+    res = ctx.zeros((max(len(thetas), 1), 2))
+    info = torch.zeros(max(len(thetas), 1), dtype=torch.int64, device=ctx.device)
+    cur = torch.cuda.current_stream(ctx.device)
+    for _, st in lanes:
+        st.wait_stream(cur)
+    for k, (g, desc, mdesc) in enumerate(gens):
+        lc, st = lanes[k % len(lanes)]
+        C, mu, x = bufs[1][k % len(lanes)]
+        s = st.cuda_stream
+        ctx.call_on(lc, "bgp_construct", _lib.BGP_TRI, ctypes.byref(desc),
+                    _ptr(X) if X is not None else None, n, None, 0, dim, b, _ptr(C), s)
+        ctx.call_on(lc, "bgp_potrf_async", _ptr(C), n, b, s)
+        ctx.call_on(lc, "bgp_construct", _lib.BGP_VEC, ctypes.byref(mdesc), None, n, None, 0, 1, b,
+                    _ptr(mu), s)
+        ctx.call_on(lc, "bgp_sub", _ptr(y.data), _ptr(mu), _ptr(x), T * b, s)
+        ctx.call_on(lc, "bgp_trsv_async", _ptr(C), n, b, _ptr(x), 0, s)
+        ctx.call_on(lc, "bgp_logdet_async", _ptr(C), n, b, _ptr(res[k, 0:1]), s)
+        ctx.call_on(lc, "bgp_sumsq_async", _ptr(x), n, _ptr(res[k, 1:2]), s)
+        ctx.call_on(lc, "bgp_info_copy", _ptr(info[k:k + 1]), s)
+    for _, st in lanes:
+        cur.wait_stream(st)
+    out = res.cpu().numpy()
+    inf = info.cpu().numpy()
+    return [(float(out[k, 0]), float(out[k, 1]), int(inf[k])) for k in range(len(thetas))]
 
 
 # ---------------------------------------------------------------------------

@@ -166,14 +166,15 @@ class TileDist:
             return np.zeros((0, 4), dtype=np.int32)
         return np.concatenate(rows).astype(np.int32)
 
-    def step_plan(self, J, slot):
+    def step_plan(self, J, slot, lookahead=True):
         """StepPlan of step J: the update by panel J of every local tile of
         columns > J (column J+1 first, gated), and, on process column
         (J+1) mod Pc, the factorization of (J+1, J+1) and the solve of this
-        rank's panel-(J+1) tiles inside the same launch."""
+        rank's panel-(J+1) tiles inside the same launch (not with
+        lookahead=False: the last step before the gathered tail)."""
         K = J + 1
         items = self.update_items(J, slot)
-        d = self.factor_tile(K)
+        d = self.factor_tile(K) if lookahead else -1
         s, c = self.my_panel(K)
         if d < 0:
             return StepPlan(items, 0, -1, K * self.b, (s, 0))
@@ -233,9 +234,15 @@ def dist_cholesky(dist, local, ops, comm):
     failing pivot stays in the device status, which skips later launches.
     """
     b, T, me = dist.b, dist.T, dist.rank
+    # tail: the last tile rows, where a step's update is shorter than the
+    # look-ahead chain on any number of GPUs, are gathered to every rank and
+    # finished there on 128 tiles (the single-GPU tail re-tiling)
+    tail = ops.tail_tiles(T) if hasattr(ops, "tail_tiles") else 0
+    J0 = T - tail if 0 < tail and 2 * tail < T else T
+    nsteps = min(T - 1, J0)
     ops.sweep_begin(T)
     layouts = [dist.panel_layout(J) for J in range(T - 1)]
-    plans = [dist.step_plan(J, layouts[J][1]) for J in range(T - 1)]
+    plans = [dist.step_plan(J, layouts[J][1], lookahead=J + 1 < J0) for J in range(nsteps)]
     dev = ops.prepare_items([p.items for p in plans])
     par_tiles = _PAR_PASS_TILES.get(b, 0)
     # fused panel exchange (the TRSM epilogue stores into every rank's panel
@@ -282,15 +289,52 @@ def dist_cholesky(dist, local, ops, comm):
     if T > 1:
         if xchg is None:
             broadcast_panel(0)
-    for J in range(T - 1):
+    for J in range(nsteps):
         if xchg is not None:
             comm.barrier_stream()  # panel J complete everywhere; buffer (J+1) % 2 free
         plan = plans[J]
         par = plan.trsm[1] > 0 and len(plan.items) <= par_tiles
-        ops.step(J, local, buffer(J, layouts[J][2]), dev[J], plan, par, push_args(J + 1))
-        if xchg is None and J + 1 < T - 1:
+        ops.step(J, local, buffer(J, layouts[J][2]), dev[J], plan, par,
+                 push_args(J + 1) if J + 1 < J0 else None)
+        if xchg is None and J + 1 < min(T - 1, J0):
             broadcast_panel(J + 1)
-    return comm.min_nonzero(ops.end())
+    info = comm.min_nonzero(ops.end())
+    if J0 < T and not info:
+        info = comm.min_nonzero(factor_tail(dist, local, ops, comm, J0))
+    return info
+
+
+def factor_tail(dist, local, ops, comm, J0):
+    """Finish the factorization of the trailing tile rows J0.. (all panels
+    < J0 applied): every rank gathers the trailing triangle (one all-gather
+    of the ranks' trailing tiles, contiguous in their column-packed
+    storage), factors it itself (ops.factor_tail: single-GPU look-ahead
+    factorization re-tiled to 128) and keeps its own tiles.  Returns the
+    failing pivot row (1-based, global) or 0."""
+    b, T = dist.b, dist.T
+    T2 = T - J0
+    G = dist.grid.G
+    shares = []
+    for r in range(G):
+        d = dist if r == dist.rank else TileDist(dist.n, b, dist.grid, r)
+        first = int(d.col_start[J0])
+        t = d.tiles[first:]
+        I2, C2 = t[:, 0].astype(np.int64) - J0, t[:, 1].astype(np.int64) - J0
+        shares.append((first, C2 * T2 - C2 * (C2 - 1) // 2 + (I2 - C2)))
+    width = max(len(idx) for _, idx in shares)
+    first, mine = shares[dist.rank]
+    part = ops.empty((max(width, 1), b, b))
+    if len(mine):
+        part[:len(mine)].copy_(local[first:first + len(mine)])
+    sub = ops.empty((T2 * (T2 + 1) // 2, b, b))
+    import torch
+    for (_, idx), piece in zip(shares, comm.all_gather(part)):
+        if len(idx):
+            sub.index_copy_(0, torch.from_numpy(idx).to(sub.device), piece[:len(idx)])
+    info = ops.factor_tail(sub, T2, dist.n - J0 * b, J0 * b)
+    if len(mine):
+        local[first:first + len(mine)].copy_(sub.index_select(0, torch.from_numpy(mine).to(sub.device)))
+    return info
 
 
 def dist_trsv(dist, local, y, ops, comm, forward=True):
@@ -696,6 +740,38 @@ class LibTileOps:
             x = PanelExchange(self.cl, comm, T)
             cache["x"] = x
         return x if x.ok else None
+
+    def tail_tiles(self, T):
+        """Trailing tile rows finished gathered on every rank:
+        about 6,000 rows, where a step's update on any number of GPUs is
+        shorter than the one-CTA POTRF + inverse chain at b = 256 / 512."""
+        return {256: 24, 384: 16, 512: 12}.get(self.b, 0)
+
+    def factor_tail(self, sub, T2, n2, row0):
+        """Factor the packed trailing triangle `sub` (T2 tile rows of b, n2
+        live rows) in place on this GPU: re-tiled to 128 and run through
+        bgp_potrf (look-ahead inside the update launches).  Returns the
+        failing row (global, 1-based) or 0."""
+        import ctypes
+
+        import torch
+        b, f = self.b, self.b // 128
+        T1 = T2 * f
+        key = (T2, b)
+        if getattr(self, "_tail_idx", (None,))[0] != key:
+            i1 = np.array([i for j in range(T1) for i in range(j, T1)])
+            j1 = np.array([j for j in range(T1) for i in range(j, T1)])
+            I, J = i1 // f, j1 // f
+            big = J * T2 - J * (J - 1) // 2 + (I - J)
+            dev = lambda a: torch.from_numpy(a).to(self.cl.device)  # noqa: E731
+            self._tail_idx = (key, dev(big), dev(j1 % f), dev(i1 % f))
+        _, big, cj, ci = self._tail_idx
+        view = sub.view(-1, f, 128, f, 128)  # [tile][cj][cc][ci][rr] (column-major tiles)
+        small = view[big, cj, :, ci, :].contiguous()
+        info = ctypes.c_int64(0)
+        self.cl.call("bgp_potrf", self._p(small), n2, 128, ctypes.byref(info), self.cl.stream)
+        view[big, cj, :, ci, :] = small
+        return row0 + int(info.value) if info.value else 0
 
     def sweep_begin(self, T):
         self._T = T

@@ -148,8 +148,49 @@ class B200Cluster:
         self._dev_inputs[cache_key] = (arr, dev)
         return dev
 
+    def input_span(self, inputs_name, keys):
+        """Upper bound on the distance between any two points of the pushed
+        coordinate arrays `keys` (their joint bounding-box diagonal), cached
+        with the arrays; lets the covariance kernel drop its underflow test."""
+        inputs = self.fetch(inputs_name)
+        arrs = tuple(inputs[k] for k in keys)
+        cache = self.__dict__.setdefault("_spans", {})
+        hit = cache.get((inputs_name, keys))
+        if hit is not None and all(a is b for a, b in zip(hit[0], arrs)):
+            return hit[1]
+        pts = [np.asarray(a, dtype=np.float64).reshape(len(a), -1) for a in arrs]
+        lo = np.min([p.min(axis=0) for p in pts], axis=0)
+        hi = np.max([p.max(axis=0) for p in pts], axis=0)
+        span = float(np.sqrt(np.sum((hi - lo) ** 2))) * (1.0 + 1e-12)
+        cache[(inputs_name, keys)] = (arrs, span)
+        return span
+
     def launches(self):
-        return int(self.lib.bgp_launch_count(self._ctx))
+        total = int(self.lib.bgp_launch_count(self._ctx))
+        for c, _ in self.__dict__.get("_lanes", []):
+            total += int(self.lib.bgp_launch_count(c))
+        return total
+
+    def lanes(self, k):
+        """k (library context, CUDA stream) pairs for pipelined work: each
+        lane has its own scratch, status and counters, so factorizations on
+        different lanes can be in flight at once (distla.loglik_many)."""
+        torch = _torch()
+        lanes = self.__dict__.setdefault("_lanes", [])
+        while len(lanes) < k:
+            c = ctypes.c_void_p()
+            if self.lib.bgp_init(self.device_index, ctypes.byref(c)) != 0:
+                raise WorkerFailure(self.rank, RuntimeError("bgp_init failed for a lane"))
+            lanes.append((c, torch.cuda.Stream(device=self.device)))
+        return lanes[:k]
+
+    def call_on(self, ctx, name, *args):
+        """A libbgp entry point on another context of this device (a lane)."""
+        rc = getattr(self.lib, name)(ctx, *args)
+        if rc != 0:
+            msg = self.lib.bgp_last_error(ctx).decode(errors="replace")
+            raise WorkerFailure(self.rank, RuntimeError(f"{name} returned {rc}: {msg}"))
+        return rc
 
     def fetch(self, name):
         try:
@@ -258,6 +299,8 @@ class B200Cluster:
                     x.close()
                 _torch().cuda.synchronize(self.device)
             finally:
+                for c, _ in self.__dict__.pop("_lanes", []):
+                    self.lib.bgp_finalize(c)
                 self.lib.bgp_finalize(self._ctx)
                 self._ctx = ctypes.c_void_p()
                 self.state = "shutdown"

@@ -44,7 +44,7 @@ def test_library_is_sm100a():
 def test_generator_struct_layout_matches_header():
     from paper_1305_4886_b200._lib import Generator
     # 4 ints + 8 + 2 doubles
-    assert ctypes.sizeof(Generator) == 4 * 4 + 10 * 8
+    assert ctypes.sizeof(Generator) == 4 * 4 + 11 * 8  # include/bgp.h bgp_generator
 
 
 def test_missing_library_fails_loudly(tmp_path):

@@ -28,9 +28,10 @@ class NumpyTileOps:
     each solved tile also copied into every rank's panel buffer (push); once
     a pivot failed, later steps are skipped (the device status)."""
 
-    def __init__(self, b, n, xchg=None):
+    def __init__(self, b, n, xchg=None, tail=0):
         self.b, self.n = b, n
         self.xchg = xchg
+        self.tail = tail
         self.info = 0
 
     def empty(self, shape):
@@ -63,6 +64,25 @@ class NumpyTileOps:
 
     def sweep_begin(self, T):
         self.info = 0
+
+    def tail_tiles(self, T):
+        return self.tail
+
+    def factor_tail(self, sub, T2, n2, row0):
+        """The gathered trailing triangle, factored densely."""
+        b = self.b
+        tiles = [(I, J) for J in range(T2) for I in range(J, T2)]
+        A = np.zeros((T2 * b, T2 * b))
+        for t, (I, J) in enumerate(tiles):
+            A[I * b:(I + 1) * b, J * b:(J + 1) * b] = self._m(sub[t])
+        A = np.tril(A)
+        try:
+            L = np.linalg.cholesky(A + np.tril(A, -1).T)
+        except np.linalg.LinAlgError:
+            return row0 + 1
+        for t, (I, J) in enumerate(tiles):
+            self._m(sub[t])[:] = L[I * b:(I + 1) * b, J * b:(J + 1) * b]
+        return 0
 
     def prepare_items(self, per_step):
         return [np.asarray(a).reshape(-1, 4) for a in per_step]
@@ -161,7 +181,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, b, q, bufs):
+def _worker(rank, world, port, n, b, q, bufs, tail=0):
     import torch
     import torch.distributed as dist
 
@@ -180,7 +200,7 @@ def _worker(rank, world, port, n, b, q, bufs):
         td = TileDist(n, b, DeviceGrid(world), rank)
         local = _local_tiles(td, P, b)
         xchg = SharedPanelExchange(bufs, rank) if bufs is not None else None
-        ops, comm = NumpyTileOps(b, n, xchg), TorchComm()
+        ops, comm = NumpyTileOps(b, n, xchg, tail), TorchComm()
         info = dist_cholesky(td, local, ops, comm)
         # gather L into a dense matrix on every rank
         Ld = torch.zeros((T * b, T * b), dtype=torch.float64)
@@ -188,9 +208,11 @@ def _worker(rank, world, port, n, b, q, bufs):
             Ld[I * b:(I + 1) * b, J * b:(J + 1) * b] = torch.from_numpy(local[k].numpy().T.copy())
         dist.all_reduce(Ld)
         # the shadow copies of the diagonal tiles factor to the owner's L
+        # (those of the gathered tail are not used)
+        J0 = T - tail if 0 < tail and 2 * tail < T else T
         shadow_ok = all(np.array_equal(np.tril(local[td.shadow_local[K]].numpy().T),
                                        Ld.numpy()[K * b:(K + 1) * b, K * b:(K + 1) * b])
-                        for K in td.shadows)
+                        for K in td.shadows if K < J0)
         ops.xchg = None
         y = torch.zeros(T * b, dtype=torch.float64)
         y[:n] = torch.from_numpy(np.random.default_rng(3).standard_normal(n))
@@ -218,15 +240,17 @@ def _shared_bufs(world, n, b):
 
 
 @pytest.mark.parametrize("xfer", ["push", "broadcast"])
-@pytest.mark.parametrize("world,n,b", [(2, 37, 8), (2, 100, 16), (4, 90, 8), (4, 37, 16),
-                                       (8, 100, 8), (8, 61, 4)])
-def test_distributed_cholesky_solves_logdet(world, n, b, xfer):
+@pytest.mark.parametrize("world,n,b,tail", [(2, 37, 8, 0), (2, 100, 16, 0), (4, 90, 8, 3), (4, 37, 16, 0),
+                                            (8, 100, 8, 4), (8, 61, 4, 0)])
+def test_distributed_cholesky_solves_logdet(world, n, b, tail, xfer):
+    """tail > 0: the last `tail` tile rows are gathered to every rank and
+    finished there (parallel.factor_tail)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     bufs = _shared_bufs(world, n, b) if xfer == "push" else None
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q, bufs)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q, bufs, tail)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=240) for _ in range(world)]

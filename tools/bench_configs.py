@@ -108,9 +108,16 @@ def c2(cl, tile):
     lib.bgp_set_profiling(ctx, 0)
     errs = [rel(a, b) for a, b in zip(lls, SURVEY["c2_ll"])]
     facts = max(prof[7], 1)
+    # the same ten evaluations pipelined (KrigeProblem.log_density_many)
+    thetas = [np.array([2.0, r, 0.05]) for r in np.linspace(0.02, 0.2, 10)]
+    prob.log_density_many([np.array([2.0, 0.0205, 0.05])])  # lane buffers
+    many, t_many = timed(lambda: prob.log_density_many(thetas))
+    errs_many = [rel(a, b) for a, b in zip(many, lls)]
     return {"config": 2, "n": n, "evals_per_s": 10 / sum(ts), "total_s": sum(ts), "ll": lls,
             "max_rel_err_vs_survey_12sf": max(errs), "tol": "12 significant digits (5e-12)",
             "tile": tile, "eval_ms": [1e3 * t for t in ts],
+            "pipelined_evals_per_s": 10 / t_many, "pipelined_total_s": t_many,
+            "pipelined_max_rel_diff_vs_sequential": max(errs_many),
             "cholesky_ms_per_eval": prof[8] / facts, "update_launch_ms_per_eval": prof[2] / facts,
             "last_factorization_step_ms": [round(steps[i], 4) for i in range(ns)]}
 
