@@ -336,6 +336,8 @@ def run_b200(args, world, rank):
         comm = {"comm_ms": max_over_ranks(c.get("comm_ms", 0.0), world),
                 "exposed_comm_ms": max_over_ranks(c.get("exposed_comm_ms", 0.0), world),
                 "collectives_per_rank": c.get("collectives", 0),
+                "rank0_step_launch_ms": c.get("step_launch_ms"),
+                "rank0_comm_span_ms": c.get("comm_span_ms"),
                 "panel_exchange": ("fused TRSM + NVLink peer stores (bgp_panel_trsm_push)"
                                    if cl.__dict__.get("_panel_xchg", {}).get("x") is not None
                                    and cl._panel_xchg["x"].ok else "NCCL broadcasts"),
@@ -472,6 +474,19 @@ def run_b200_c5(args, world, rank):
     ld = distla.log_det_from_chol(cl, L)
     cl.remote_rm("c5.L")
     tflops = args.steps * n ** 3 / 3 / (ms_max / 1e3) / 1e12
+    # independent check: the same kernel and recipe at n = 16,384 against the
+    # REFERENCE's logdet (tests/golden/full_configs.json, make_full_configs.py)
+    with open(os.path.join(ROOT, "tests", "golden", "full_configs.json")) as f:
+        ref_small = json.load(f)["c5s"]
+    ns = ref_small["n"]
+    Xs = np.random.default_rng(0).uniform(0, 1, (ns, 2))  # the C5 recipe's first ns points
+    lays = distla.make_layout(ns, cl.grid)
+    cl.push("c5s.inputs", {"coords": Xs})
+    distla.construct_distributed(cl, "c5s.C", "triangular", spec.cov_fn, theta,
+                                 inputs_name="c5s.inputs", row_layout=lays)
+    Ls, _ = distla.distributed_cholesky(cl, distla.DistTriangular("c5s.C", lays), "c5s.L")
+    ld_small = distla.log_det_from_chol(cl, Ls)
+    cl.remote_rm("c5s.L")
     comm = None
     if world > 1:
         cl.comm_timeline = True
@@ -510,6 +525,9 @@ def run_b200_c5(args, world, rank):
                          "frac": tflops / (FP64_DMMA_PEAK * world), "traffic": None},
             "parity": {"logdet": ld, "ref_logdet_1gpu": C5_LOGDET_1GPU,
                        "rel_err": abs(ld - C5_LOGDET_1GPU) / abs(C5_LOGDET_1GPU), "tol": 1e-10,
+                       "reference_n16384": {"logdet": ld_small, "ref_logdet": ref_small["logdet"],
+                                            "rel_err": abs(ld_small - ref_small["logdet"])
+                                            / abs(ref_small["logdet"]), "tol": 1e-12},
                        "note": "the CPU reference cannot hold C5; reference = this library on 1 GPU"},
             "clocks": clk, "gpu_launches": launches,
             "e2e": {"value": n ** 3 / 3 / e2e_s / 1e12, "unit": "TFLOP/s",

@@ -324,6 +324,10 @@ int bgp_dist_step(bgp_ctx_t ctx, int J, double* local, int64_t nlocal,
  * (stands in for the reference's event log, bg/transport/base.py:121-123). */
 #define BGP_PROFILE_SLOTS 10
 int bgp_set_profiling(bgp_ctx_t ctx, int on);
+/* GEMM launches of this context use at most max_ctas CTAs (0: all SMs) --
+ * pipelined evaluations on several contexts leave SMs to each other's
+ * latency-bound steps. */
+int bgp_set_grid_cap(bgp_ctx_t ctx, int max_ctas);
 int bgp_profile_read(bgp_ctx_t ctx, double* out);
 /* per-step trailing-update launch times (ms) of the last profiled bgp_potrf;
  * returns the number written (<= max) */

@@ -96,6 +96,7 @@ SIGNATURES = {
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), _c_dp]),
     "bgp_set_profiling": (_int, [ctypes.c_void_p, _int]),
     "bgp_set_tail": (_int, [ctypes.c_void_p, _int]),
+    "bgp_set_grid_cap": (_int, [ctypes.c_void_p, _int]),
     "bgp_profile_read": (_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "bgp_profile_steps": (_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _int]),
 }

@@ -54,7 +54,8 @@ struct Ctx {
   unsigned queue_next = 0;
   double* d_tail[2] = {nullptr, nullptr};  // re-tiled trailing triangles of the Cholesky tail
   size_t tail_cap[2] = {0, 0};
-  int dist_T = 0, dist_b = 0;  // bgp_dist_begin: tile rows and tile size of the current sweep
+  int dist_T = 0, dist_b = 0;
+  int grid_cap = 0;  // > 0: GEMM launches of this context use at most this many CTAs (bgp_set_grid_cap)  // bgp_dist_begin: tile rows and tile size of the current sweep
   int tail_tiles = 32;  // 512-tile rows finished on 256 tiles (half as many 256 rows on 128; bgp_set_tail)
   void* encode_fn = nullptr;  // cuTensorMapEncodeTiled
   // profiling (bgp_set_profiling / bgp_profile_read)

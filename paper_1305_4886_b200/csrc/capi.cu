@@ -535,6 +535,12 @@ int bgp_info_copy(bgp_ctx_t ctx, int64_t* dev_out, void* stream) {
   return e == cudaSuccess ? BGP_OK : set_err(ctx, "status copy", e);
 }
 
+int bgp_set_grid_cap(bgp_ctx_t ctx, int max_ctas) {
+  if (max_ctas < 0) return BGP_E_ARG;
+  ctx->grid_cap = max_ctas;
+  return BGP_OK;
+}
+
 int bgp_set_tail(bgp_ctx_t ctx, int tiles) {
   if (tiles < 0) return BGP_E_ARG;
   ctx->tail_tiles = tiles;

@@ -875,7 +875,8 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   for (int d = 0; d < p.npush; ++d)
     if ((rc = make_tile_map(ctx, &pm.map[d], p.push_dst[d], p.b, p.push_tiles, 16, WN, true)) != BGP_OK) return rc;
   prepare();
-  const int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
+  int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
+  if (ctx->grid_cap > 0 && ctx->grid_cap < slots) slots = ctx->grid_cap;
   int64_t grid = (tasks + GROUPS - 1) / GROUPS < slots ? (tasks + GROUPS - 1) / GROUPS : slots;
   if (p.potrf_tile && grid < 2) grid = 2;  // the look-ahead CTA must not be the only one
   // the look-ahead CTA's device POTRF / inverse must fit the ring memory

@@ -327,6 +327,10 @@ def loglik_many(ctx, thetas, cov_fn, mean_fn, inputs_name, y_name, row_layout, l
         for _, desc, _ in gens:
             desc.span = span
     lanes = ctx.lanes(max(1, int(lanes)))
+    import os
+    reserve = int(os.environ.get("BGP_LANE_RESERVE", "0"))  # SMs each lane leaves to the others
+    for lc, _ in lanes:
+        ctx.lib.bgp_set_grid_cap(lc, ctx.num_sms - reserve if reserve and len(lanes) > 1 else 0)
     key = (n, b, len(lanes))
     bufs = ctx.__dict__.get("_many_bufs")
     if bufs is None or bufs[0] != key:

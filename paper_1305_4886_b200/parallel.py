@@ -449,8 +449,13 @@ class Timeline:
         for kind, e0, e1 in self.spans:
             iv[kind].append((self._origin.elapsed_time(e0), self._origin.elapsed_time(e1)))
         comm = sum(b - a for a, b in iv["comm"])
+        # per step, in issue order: each step launch ("compute") and each
+        # barrier / broadcast ("comm") -- a step whose launch is short and
+        # whose barrier long waited for another rank or for its own chain
         return {"comm_ms": comm, "collectives": len(iv["comm"]),
-                "exposed_comm_ms": exposed_time(iv["comm"], iv["compute"])}
+                "exposed_comm_ms": exposed_time(iv["comm"], iv["compute"]),
+                "step_launch_ms": [round(b - a, 4) for a, b in iv["compute"]],
+                "comm_span_ms": [round(b - a, 4) for a, b in iv["comm"]]}
 
 
 class TorchComm:

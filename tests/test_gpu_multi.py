@@ -213,6 +213,9 @@ class _OneRank:
     def min_nonzero(self, v):
         return int(v)
 
+    def all_gather(self, t):
+        return [t]
+
 
 @pytest.mark.parametrize("tile,nt", [(128, 11), (256, 5), (512, 3), (256, 52), (512, 27)])
 @pytest.mark.parametrize("push", [True, False])

@@ -113,10 +113,13 @@ def c2(cl, tile):
     prob.log_density_many([np.array([2.0, 0.0205, 0.05])])  # lane buffers
     many, t_many = timed(lambda: prob.log_density_many(thetas))
     errs_many = [rel(a, b) for a, b in zip(many, lls)]
+    prob.log_density_many([np.array([2.0, 0.0205, 0.05])], lanes=3)
+    _, t_many3 = timed(lambda: prob.log_density_many(thetas, lanes=3))
     return {"config": 2, "n": n, "evals_per_s": 10 / sum(ts), "total_s": sum(ts), "ll": lls,
             "max_rel_err_vs_survey_12sf": max(errs), "tol": "12 significant digits (5e-12)",
             "tile": tile, "eval_ms": [1e3 * t for t in ts],
             "pipelined_evals_per_s": 10 / t_many, "pipelined_total_s": t_many,
+            "pipelined3_evals_per_s": 10 / t_many3,
             "pipelined_max_rel_diff_vs_sequential": max(errs_many),
             "cholesky_ms_per_eval": prof[8] / facts, "update_launch_ms_per_eval": prof[2] / facts,
             "last_factorization_step_ms": [round(steps[i], 4) for i in range(ns)]}

@@ -1,15 +1,19 @@
-"""Small runs of every dataflow kernel path, for compute-sanitizer.
+"""Small runs of every dataflow kernel path under the checked build.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_small.py
-    (racecheck, synccheck likewise; one tool per call)
+    make checked
+    BGP_LIB_PATH=build/checked/libbgp.so python tools/sanitize_small.py
+
+(compute-sanitizer is closed on this GPU pool; the checked build's BGP_CHECK
+bounds / invariant checks trap on a bad tile coordinate, slot or gate.)
 
 Covers: the single-GPU look-ahead factorization (update launches with the
 in-launch POTRF / inverse / gated TRSM, both TRSM regimes, the tail
 re-tiling) at tiles 128, 256 and 512; the kriging solve (bgp_trsm_rect
 with its gated fused solve); the distributed sweep step (bgp_dist_step with
 shadow tiles, the in-launch factor + solve and the panel push epilogue into
-a destination buffer -- here this process's own) on a 1 x 1 grid; the
-forward solve and the covariance kernels.  Every result is checked against
+a destination buffer -- here this process's own) on a 1 x 1 grid, with the
+gathered tail (parallel.factor_tail) at tile 256; the forward solve and the
+covariance kernels.  Every result is checked against
 numpy so a silent corruption fails the run too.
 """
 
@@ -74,6 +78,9 @@ def dist_sweep(cl, A):
         def min_nonzero(self, v):
             return int(v)
 
+        def all_gather(self, t):
+            return [t]
+
     n, b = len(A), cl.tile
     td = TileDist(n, b, DeviceGrid(1), 0)
     T = td.T
@@ -117,6 +124,10 @@ def main():
             V = distla.triangular_solve(cl, L, Rd, "V", side="forward")
             check(f"trsm_rect tile {tile}", relerr(distla.collect(cl, V), np.linalg.solve(Lref, R)), 1e-12)
             check(f"dist step tile {tile}", relerr(dist_sweep(cl, A), Lref), 1e-12)
+            if tile == 256:  # enough tile rows for the gathered tail (24 at 256)
+                At = cov(52 * 256 - 19, 7)
+                check("dist step + gathered tail tile 256", relerr(dist_sweep(cl, At), np.linalg.cholesky(At)),
+                      1e-12)
             # covariance kernels (fast interior path and the generic one)
             X = np.random.default_rng(3).uniform(0, 1, (n, 2))
             cl.push("inp", {"coords": X, "nu": 0.5})
