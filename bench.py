@@ -565,7 +565,10 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tile", type=int, default=512)
+    ap.add_argument("--tile", type=int, default=None,
+                    help="device tile size (default: 512 on one GPU; 256 on several, where the "
+                         "one-CTA POTRF + inverse chain of each step -- 4x shorter at 256 -- is "
+                         "exposed once a rank's share of the step's update gets small)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-samples", type=int, default=30)  # ~11 s of host work
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -581,6 +584,8 @@ def main():
     if env_world == 1 and args.gpus > 1 and args.impl == "b200":
         launch_ranks(args)  # does not return
     world, rank = dist_setup(args.impl, args.debug_share_gpu)
+    if args.tile is None:
+        args.tile = 512 if world == 1 else 256
     if args.impl == "reference":
         run_reference(args, world, rank)
     elif args.workload == "c5":

@@ -184,6 +184,9 @@ struct GemmProblem {
   // zeroed int: the first CTA to take a ticket is the look-ahead CTA
   // (null: launch_gemm provides one)
   int* role_ticket;
+  // GEMM_CHOL_TRAIL: live rows of the triangle (rows >= n_live are identity
+  // padding); blocks and TRSM slabs wholly in the padding are skipped (0: none)
+  int64_t n_live;
   // tile counts behind the A / B / C tensor maps (set by launch_gemm; the
   // checked build asserts every tile index against them)
   int64_t nA, nB, nC;

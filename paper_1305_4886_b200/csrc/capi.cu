@@ -322,6 +322,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     p.check_info = true;
     p.queue = gate + stride - 2;
     p.role_ticket = gate + T + 1;
+    p.n_live = n;
     const bool next = K < J_stop;  // panel K is factored here
     if (la_mode == 1) {
       if (next) {

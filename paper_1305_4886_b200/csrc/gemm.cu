@@ -91,6 +91,7 @@ struct Item {
   int gate;                  // >= 0: column-gate index this block signals (update of column J+1)
   int slab, pass;            // trsm_par TRSM pass: slab index, pass (0 = rightmost); else slab = -1
   bool valid;
+  bool pad;                  // skipped: every row lies in the identity padding (its gate still counts)
 };
 
 __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
@@ -203,6 +204,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   it.aStride = it.bStride = 0;
   it.nkt = 1;
   it.valid = true;
+  it.pad = false;
   it.lower = 0;
   it.bTriRow = -1;
   it.kstages = 0;
@@ -226,6 +228,12 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
                            : p.mode == GEMM_RECT_TRAIL                       ? (int64_t)(p.J + 1) * p.Tm
                                                                              : tri_index(p.J + 2, p.J + 1, p.T);
     trsm_block(it, p, idx, pass, panel0);
+    // Cholesky sweep: slabs of the last tile row that lie wholly in the
+    // padding hold zeros and solve to zeros -- skipped
+    if (p.mode == GEMM_CHOL_TRAIL && p.n_live > 0 &&
+        (int64_t)(p.J + 2 + (int)(idx / (p.b / BM))) == p.T - 1 &&
+        (int64_t)(p.T - 1) * p.b + it.mrow0 >= p.n_live)
+      it.valid = false, it.pad = true;
     return it;
   }
   const int64_t t = idx / nblk;
@@ -243,6 +251,11 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
       it.bTile0 = tri_index(C, p.J, p.T);
       if (R == C) diag_block(it, bi, bj);
       if (cc == 0 && p.col_gate) it.gate = rr;  // column J+1: POTRF / TRSM of the next panel wait on it
+      // blocks of the last tile row wholly in the identity padding: their
+      // panel rows are zero, so the update is exactly zero -- skipped (about
+      // 1.4 % of the flops at C4, b = 512)
+      if (p.n_live > 0 && R == p.T - 1 && (int64_t)R * p.b + it.mrow0 >= p.n_live && it.valid)
+        it.valid = false, it.pad = true;
       break;
     }
     case GEMM_RECT_TRAIL: {
@@ -406,7 +419,11 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
     const int npass = gemm_task_passes(p, task);
     for (int pass = 0; pass < npass; ++pass) {
       const Item it = gemm_decode(p, task, pass);
-      if (!it.valid) continue;
+      if (!it.valid) {
+        // a padding block counts toward its tile's gate as if it had retired
+        if (it.pad && it.gate >= 0) atomicAdd(p.col_gate + it.gate, GROUP_WARPS);
+        continue;
+      }
       const CUtensorMap* tb = it.bLinv ? tmL : tmB;
       const CUtensorMap* ta = (it.bLinv && !p.trsm_oop) ? tmT : tmA;
       const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
