@@ -50,7 +50,9 @@ def _worker(rank, world, port, q, xfer="push"):
         lay = distla.make_layout(n, cl.grid, h=2)
         C = distla.distribute(cl, "C", A, "triangular", lay)
         cl.comm_timeline = True  # CUDA-event spans of broadcasts and updates
+        launches = cl.launches()
         L, stats = distla.distributed_cholesky(cl, C, "L")
+        out["chol_launches"] = cl.launches() - launches
         cl.comm_timeline = False
         out["comm"] = cl.last_comm
         x = cl.__dict__.get("_panel_xchg", {}).get("x")
@@ -133,6 +135,10 @@ def test_multi_rank_path_on_one_gpu(world, xfer):
         assert abs(r["logdet"] - np.linalg.slogdet(A)[1]) <= 1e-12 * abs(r["logdet"])
         assert r["npd"] == 1 and "Ln" not in r["ls"] and "Cn" not in r["ls"]
         assert r["xfer"] == xfer
+        # the panel solve and its exchange run inside the step launches: one
+        # launch per step (+ panel 0's factor and solve), nothing on the side
+        assert r["chol_launches"] <= T + 1
+        assert len(r["comm"]["step_launch_ms"]) <= T - 1
         c = r["comm"]
         assert c["collectives"] > 0 and 0.0 <= c["exposed_comm_ms"] <= c["comm_ms"] + 1e-6
         assert abs(r["ll"] - want_ll) <= 1e-10 * abs(want_ll)
