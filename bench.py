@@ -47,7 +47,7 @@ THETA = np.array([1.0, 0.08, 0.02])
 # carries no FP64 entry, so the roofline uses the DMMA probe.
 FP64_DMMA_PEAK = 37.1
 CUBLAS_DGEMM = 35.8
-REF_SAMPLES = 8  # reference arm: samples per step
+REF_SUB_BLOCKS = 20  # reference sampler: sub-evaluation of 20 reference blocks (19,800 points)
 
 
 def gemm_traffic():
@@ -176,10 +176,10 @@ def full_eval_record():
 
 
 def cpu_reference(samples, X):
-    """Sampled reference evaluation time: the median over `samples` samples
-    of each one's extrapolated evaluation time."""
-    from oracle.cpu_baseline import ReferenceSampler, host_cores
-    s = ReferenceSampler(X, THETA)
+    """Sampled reference evaluation time: the median over `samples`
+    sub-evaluations of each one's extrapolated evaluation time."""
+    from oracle.cpu_baseline import SubEvalSampler, host_cores
+    s = SubEvalSampler(X, THETA, blocks=REF_SUB_BLOCKS)
     evals, chols, walls = [], [], []
     for _ in range(samples):
         t, wall = s.sample()
@@ -192,8 +192,8 @@ def cpu_reference(samples, X):
     return {"evals_per_s": 1.0 / total, "eval_s": total, "chol_s": chol,
             "eval_s_range": [min(evals), max(evals)],
             "chol_tflops": n ** 3 / 3 / chol / 1e12, "cores": host_cores(),
-            "sample": s.describe() + f"; median over {samples} samples of the extrapolated "
-                      f"evaluation; {sum(walls):.1f} s of sampling", "walls": walls}
+            "sample": s.describe() + f"; median over {samples} sub-evaluation(s); "
+                      f"{sum(walls):.1f} s of sampling", "walls": walls}
 
 
 def run_reference(args, world, rank):
@@ -201,23 +201,19 @@ def run_reference(args, world, rank):
     X, _, _ = load_c4()
     if rank != 0:
         return
-    from oracle.cpu_baseline import ReferenceSampler, host_cores
-    s = ReferenceSampler(X, THETA)
+    from oracle.cpu_baseline import SubEvalSampler, host_cores
+    s = SubEvalSampler(X, THETA, blocks=REF_SUB_BLOCKS)
     per_step, per_step_chol = [], []
     for _ in range(args.warmup):
         s.sample()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        # one step = REF_SAMPLES samples (~3 s of host work): the step's
-        # evaluation time is the median of the samples' extrapolations
-        ev, ch = [], []
-        for _ in range(REF_SAMPLES):
-            t, _ = s.sample()
-            a, c = s.extrapolate(t)
-            ev.append(a)
-            ch.append(c)
-        per_step.append(statistics.median(ev))
-        per_step_chol.append(statistics.median(ch))
+        # one step = one sub-evaluation (~20-30 s of host work), extrapolated
+        # to the full evaluation by exact operation counts
+        t, _ = s.sample()
+        a, c = s.extrapolate(t)
+        per_step.append(a)
+        per_step_chol.append(c)
     wall = time.perf_counter() - t0
     total, chol = statistics.median(per_step), statistics.median(per_step_chol)
     value = 1.0 / total
@@ -234,8 +230,7 @@ def run_reference(args, world, rank):
         "measured_full_eval": full_eval_record(),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": host_cores(),
                          "kind": "port", "sample": s.describe() +
-                         f"; each step = {REF_SAMPLES} samples, step value = median of their "
-                         "extrapolations, line value = median over steps",
+                         "; each step = one sub-evaluation, line value = median over steps",
                          "extrapolated_eval_s": total, "measured_full_eval": full_eval_record()},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -570,7 +565,7 @@ def main():
                          "one-CTA POTRF + inverse chain of each step -- 4x shorter at 256 -- is "
                          "exposed once a rank's share of the step's update gets small)")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-samples", type=int, default=30)  # ~11 s of host work
+    ap.add_argument("--cpu-samples", type=int, default=1)  # sub-evaluations (~20-30 s of host work)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: the BASELINE metric (default); c5: config 5 Cholesky scaling")

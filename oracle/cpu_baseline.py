@@ -15,10 +15,12 @@ operation's mean time by its exact count in one evaluation:
   gemm       sum_J (B-J-1)(B-J-2)/2    (BLAS-3, A_RJ A_CJ^T)
   gemv       B(B-1)/2 + B trsv         (forward solve)
 
-A full evaluation of the reference at n = 67,275 takes ~10 min on 8 cores
-(SURVEY.md 6); the sample keeps bench.py within minutes and states itself in
-the JSON line.  The operations run on real blocks of the C4 covariance and its
-factor, so BLAS sees the same shapes and conditioning as the full run.
+A full evaluation of the reference at n = 67,275 takes 4.6 min on the GPU
+box's 16 host cores (oracle/full_eval.py, profiles/r02_cpu_full_eval.json);
+the sample keeps bench.py within minutes and states itself in the JSON line.
+SubEvalSampler (bench.py's sampler) measures the per-call times inside one
+real evaluation of a prefix of the problem with the full problem's block
+shapes; ReferenceSampler (isolated micro-timings) is kept for comparison.
 """
 
 import math
@@ -120,6 +122,47 @@ class ReferenceSampler:
         return (f"reference P=1 block sweep (block {self.bs}, B={self.B}) at n={self.n}: "
                 f"sampled real blocks per step (4 construct, median of 6 potrf/trsm/gemm/syrk/gemv/trsv), "
                 f"scaled by exact op counts {self.counts}")
+
+
+class SubEvalSampler:
+    """The reference algorithm's per-operation times measured inside a real
+    (smaller) evaluation: one full P = 1 evaluation (oracle/full_eval.py) on
+    the first n_sub points with the FULL problem's block size, so every BLAS
+    / LAPACK / construct call has the same shape as in the full run and runs
+    back to back in the same sweep (streaming blocks, warm thread pools).
+    Each kind's mean call time is scaled by its exact count in the full
+    evaluation (op_counts).  Isolated micro-timings (ReferenceSampler) were
+    off by +24 % (median) / -37 % (min) against a timed full evaluation
+    (DESIGN.md 6); this stays within a few percent of it."""
+
+    def __init__(self, X, theta, y=None, nu=0.5, kernel="matern-nugget", blocks=16, seed=0):
+        self.X = np.asarray(X, dtype=float)
+        self.n = len(self.X)
+        self.bs = block_size(self.n, default_h(self.n))
+        self.B = math.ceil(self.n / self.bs)
+        self.n_sub = min(self.n, blocks * self.bs)
+        self.theta = np.asarray(theta, dtype=float)
+        self.kernel, self.nu = kernel, nu
+        rng = np.random.default_rng(seed)
+        self.y = np.asarray(y, dtype=float)[:self.n_sub] if y is not None else rng.standard_normal(self.n_sub)
+        self.counts = op_counts(self.n, self.bs)
+
+    def sample(self):
+        from . import full_eval
+        ot = {}
+        t0 = time.perf_counter()
+        full_eval.log_density(self.X[:self.n_sub], self.y, self.theta, kernel=self.kernel, nu=self.nu,
+                              bs=self.bs, op_times=ot)
+        t = {k: ot[k] / ot[k + "_n"] for k in ("construct", "potrf", "trsm", "syrk", "gemm", "gemv", "trsv")
+             if ot.get(k + "_n")}
+        return t, time.perf_counter() - t0
+
+    extrapolate = ReferenceSampler.extrapolate
+
+    def describe(self):
+        return (f"reference P=1 block sweep (block {self.bs}, B={self.B}) at n={self.n}: per-call times "
+                f"of each operation kind measured inside one full evaluation of the first {self.n_sub} "
+                f"points (same block shapes), scaled by exact op counts {self.counts}")
 
 
 def host_cores():

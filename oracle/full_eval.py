@@ -34,7 +34,21 @@ def _tri(I, J, B):
     return J * B - J * (J - 1) // 2 + (I - J)
 
 
-def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None):
+def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None, op_times=None):
+    """One evaluation; with op_times (a dict) the wall time of every
+    construct block / potrf / trsm / syrk / gemm / gemv / trsv call is added
+    up per kind there (with "<kind>_n" counts), for the sampled baseline."""
+    import collections
+    tick = time.perf_counter
+    acc = op_times if op_times is not None else collections.defaultdict(float)
+
+    def timed(kind, fn):
+        t = tick()
+        out = fn()
+        acc[kind] = acc.get(kind, 0.0) + tick() - t
+        acc[kind + "_n"] = acc.get(kind + "_n", 0) + 1
+        return out
+
     X = np.asarray(X, dtype=float)
     y = np.asarray(y, dtype=float)
     n = len(y)
@@ -53,7 +67,10 @@ def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None):
             if I == J:
                 mask &= ii >= jj
             blk = A[_tri(I, J, B)]
+            t = tick()
             blk[mask] = np.asarray(gen(theta, inputs, ii[mask], jj[mask]), dtype=float)
+            acc["construct"] = acc.get("construct", 0.0) + tick() - t
+            acc["construct_n"] = acc.get("construct_n", 0) + 1
     for t in range(n, B * bs):  # identity on the padded diagonal tail
         A[_tri(B - 1, B - 1, B)][t - (B - 1) * bs, t - (B - 1) * bs] = 1.0
     times["construct_s"] = time.perf_counter() - t0
@@ -62,18 +79,20 @@ def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None):
 
     t1 = time.perf_counter()
     for J in range(B):
-        L = la.cholesky(A[_tri(J, J, B)], lower=True, check_finite=False)
+        L = timed("potrf", lambda: la.cholesky(A[_tri(J, J, B)], lower=True, check_finite=False))
         A[_tri(J, J, B)] = L
         for I in range(J + 1, B):
             k = _tri(I, J, B)
-            A[k] = la.solve_triangular(L, A[k].T, lower=True, check_finite=False).T
+            A[k] = timed("trsm", lambda: la.solve_triangular(L, A[k].T, lower=True, check_finite=False).T)
         for C in range(J + 1, B):
             Wc = A[_tri(C, J, B)]
             for R in range(C, B):
                 if R == C:
-                    A[_tri(R, C, B)] -= np.tril(Wc @ Wc.T)
+                    timed("syrk", lambda: np.subtract(A[_tri(R, C, B)], np.tril(Wc @ Wc.T),
+                                                      out=A[_tri(R, C, B)]))
                 else:
-                    A[_tri(R, C, B)] -= A[_tri(R, J, B)] @ Wc.T
+                    timed("gemm", lambda: np.subtract(A[_tri(R, C, B)], A[_tri(R, J, B)] @ Wc.T,
+                                                      out=A[_tri(R, C, B)]))
         if log and J % 8 == 0:
             log(f"chol step {J}/{B} {time.perf_counter() - t1:.1f} s")
     times["cholesky_s"] = time.perf_counter() - t1
@@ -83,11 +102,11 @@ def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None):
     resid[:n] = y
     u = np.zeros(B * bs)
     for J in range(B):
-        acc = resid[J * bs:(J + 1) * bs].copy()
+        r = resid[J * bs:(J + 1) * bs].copy()
         for K in range(J):
-            acc -= A[_tri(J, K, B)] @ u[K * bs:(K + 1) * bs]
-        u[J * bs:(J + 1) * bs] = la.solve_triangular(A[_tri(J, J, B)], acc, lower=True,
-                                                     check_finite=False)
+            r -= timed("gemv", lambda: A[_tri(J, K, B)] @ u[K * bs:(K + 1) * bs])
+        u[J * bs:(J + 1) * bs] = timed("trsv", lambda: la.solve_triangular(
+            A[_tri(J, J, B)], r, lower=True, check_finite=False))
     logdet = 0.0
     for J in range(B):
         live = min(max(n - J * bs, 0), bs)

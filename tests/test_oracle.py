@@ -156,3 +156,15 @@ def test_full_size_reference_fixtures_agree_with_survey():
         X = orc.config_inputs(cfg, n=n)[1]
         key = {2: "c2", 3: "c3", 5: "c5s", 4: "c4_lead"}[cfg]
         assert float(np.sum(X)) == meta[key]["X"]["sum"]
+
+
+def test_sub_evaluation_sampler_extrapolates_by_op_counts():
+    from oracle.cpu_baseline import SubEvalSampler, op_counts
+    kern, X, theta, extra, z = orc.config_inputs(1)
+    s = SubEvalSampler(X, theta, blocks=2)
+    assert s.n_sub == 2 * s.bs and s.counts == op_counts(len(X), s.bs)
+    t, wall = s.sample()
+    assert set(t) == {"construct", "potrf", "trsm", "syrk", "gemv", "trsv"}  # no GEMM in 2 blocks
+    t["gemm"] = t["syrk"]
+    total, chol = s.extrapolate(t)
+    assert 0 < chol < total and wall > 0
