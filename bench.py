@@ -162,17 +162,23 @@ def max_over_ranks(x, world):
 
 
 def full_eval_record():
-    """A timed FULL reference-algorithm evaluation at C4 on a GPU box's host
+    """Timed FULL reference-algorithm evaluations at C4 on a GPU box's host
     (tools/cpu_full_eval.py, committed under profiles/), reported beside the
     sampler's extrapolation; None if none is committed."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_cpu_full_eval.json")))
     if not files:
         return None
-    with open(files[-1]) as f:
-        rec = json.load(f)
-    rec["file"] = os.path.relpath(files[-1], ROOT)
-    return rec
+    runs = []
+    for f in files:
+        with open(f) as fh:
+            rec = json.load(fh)
+        runs.append({"file": os.path.relpath(f, ROOT), "eval_s": rec["eval_s"],
+                     "construct_s": rec["construct_s"], "cholesky_s": rec["cholesky_s"],
+                     "ll_rel_err": rec["ll_rel_err"]})
+    mean = statistics.mean(r["eval_s"] for r in runs)
+    return {"what": rec["what"], "n": rec["n"], "cores_used": rec["cores_used"], "lscpu": rec["lscpu"],
+            "runs": runs, "eval_s_mean": mean, "evals_per_s": 1.0 / mean}
 
 
 def cpu_reference(samples, X):

@@ -36,17 +36,15 @@ def _tri(I, J, B):
 
 def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None, op_times=None):
     """One evaluation; with op_times (a dict) the wall time of every
-    construct block / potrf / trsm / syrk / gemm / gemv / trsv call is added
-    up per kind there (with "<kind>_n" counts), for the sampled baseline."""
-    import collections
+    construct block / potrf / trsm / syrk / gemm / gemv / trsv call is
+    appended per kind there (lists of seconds), for the sampled baseline."""
     tick = time.perf_counter
-    acc = op_times if op_times is not None else collections.defaultdict(float)
+    acc = op_times if op_times is not None else {}
 
     def timed(kind, fn):
         t = tick()
         out = fn()
-        acc[kind] = acc.get(kind, 0.0) + tick() - t
-        acc[kind + "_n"] = acc.get(kind + "_n", 0) + 1
+        acc.setdefault(kind, []).append(tick() - t)
         return out
 
     X = np.asarray(X, dtype=float)
@@ -69,8 +67,7 @@ def log_density(X, y, theta, kernel="matern-nugget", nu=0.5, bs=None, log=None, 
             blk = A[_tri(I, J, B)]
             t = tick()
             blk[mask] = np.asarray(gen(theta, inputs, ii[mask], jj[mask]), dtype=float)
-            acc["construct"] = acc.get("construct", 0.0) + tick() - t
-            acc["construct_n"] = acc.get("construct_n", 0) + 1
+            acc.setdefault("construct", []).append(tick() - t)
     for t in range(n, B * bs):  # identity on the padded diagonal tail
         A[_tri(B - 1, B - 1, B)][t - (B - 1) * bs, t - (B - 1) * bs] = 1.0
     times["construct_s"] = time.perf_counter() - t0
