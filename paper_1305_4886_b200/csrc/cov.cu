@@ -156,6 +156,48 @@ __device__ __forceinline__ double cov_fast(double q, double sc, const double* __
   return fma(fma(sv, 1.0 / 3.0, 1.0) * sv, e, e);
 }
 
+// Fast path of one tile: a thread owns rows r, r+1 (their points in
+// registers) over a contiguous share of the columns, reads each column point
+// once from shared memory and writes both entries with one 16-byte store.
+// DIAG: strict upper triangle zero, nugget where i == j.  PAD: rows / columns
+// past n are the identity padding (their point loads are clamped, the values
+// masked).
+template <int KIND, bool DIAG, bool PAD>
+__device__ __forceinline__ void cov_tile_fast(const GenDev& g, const double* __restrict__ X, int64_t n, int b,
+                                              int64_t i0, int64_t j0, const double* colpts,
+                                              const double* __restrict__ tab, double* tile) {
+  const int npairs = b / 2, nsplit = blockDim.x / npairs;
+  const int pr = threadIdx.x % npairs, part = threadIdx.x / npairs;
+  if (part >= nsplit) return;
+  const int r = 2 * pr, cw = b / nsplit, c0 = part * cw;
+  const int64_t ia = i0 + r, ib = ia + 1;
+  const double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ia, n - 1) : ia));
+  const double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ib, n - 1) : ib));
+  const double sc = (KIND & 7) == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
+  const double tau2 = (g.nugget && g.part == BGP_PART_COV) ? g.p[g.np - 1] : 0.0;
+  const double2* cp = reinterpret_cast<const double2*>(colpts);
+  double2* dst = reinterpret_cast<double2*>(tile + r);
+#pragma unroll kCovUnroll
+  for (int c = c0; c < c0 + cw; ++c) {
+    const double2 pc = cp[c];
+    const double ax = x0.x - pc.x, ay = x0.y - pc.y;
+    const double bx = x1.x - pc.x, by = x1.y - pc.y;
+    double2 v;
+    v.x = cov_fast<KIND>(fma(ax, ax, ay * ay), sc, tab);
+    v.y = cov_fast<KIND>(fma(bx, bx, by * by), sc, tab);
+    if (DIAG) {  // rows r, r+1 of a diagonal tile: lower part, nugget where i == j
+      v.x = c > r ? 0.0 : (c == r ? v.x + tau2 : v.x);
+      v.y = c > r + 1 ? 0.0 : (c == r + 1 ? v.y + tau2 : v.y);
+    }
+    if (PAD) {  // identity padding (bg/distla/objects.py:60-80)
+      const int64_t j = j0 + c;
+      if (ia >= n || j >= n) v.x = (ia == j) ? 1.0 : 0.0;
+      if (ib >= n || j >= n) v.y = (ib == j) ? 1.0 : 0.0;
+    }
+    __stcs(dst + (int64_t)c * (b / 2), v);
+  }
+}
+
 // triangular: one CTA per lower tile (flat packed index, or an explicit
 // (I, J) list for a rank's share of a 2-D block-cyclic distribution)
 template <bool kPts, int KIND>
@@ -180,37 +222,21 @@ __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const do
     colpts[t] = (kPts && jj < n) ? X[jj * dim + t % dim] : 0.0;
   }
   // interior tiles (no padding, off the diagonal): no per-entry checks
-  // tiles without padding (all but the last tile row) take the fast path;
-  // on diagonal tiles it masks the strict upper triangle and adds the nugget
-  const bool interior = KIND != 0 && i0 + b <= n && j0 + b <= n;
-  if (interior && threadIdx.x < 64) tab[threadIdx.x] = g.p[0] * kExp2Tab[threadIdx.x];
+  // every tile of a 2-D built-in kernel takes the fast path (cov_tile_fast);
+  // diagonal tiles mask their strict upper triangle and add the nugget,
+  // tiles of the last tile row mask the identity padding
+  const bool fast = KIND != 0;
+  if (fast && threadIdx.x < 64) tab[threadIdx.x] = g.p[0] * kExp2Tab[threadIdx.x];
   __syncthreads();
   double* tile = out + (int64_t)blockIdx.x * b * b;
-  if (interior) {
-    // thread -> row pair (t mod b/2) over a contiguous share of the columns
-    const int npairs = b / 2, nsplit = blockDim.x / npairs;
-    const int pr = threadIdx.x % npairs, part = threadIdx.x / npairs;
-    if (part >= nsplit) return;
-    const int r = 2 * pr, cw = b / nsplit, c0 = part * cw;
-    const double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r));
-    const double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (i0 + r + 1));
-    const double sc = (KIND & 7) == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
-    const double tau2 = (g.nugget && g.part == BGP_PART_COV) ? g.p[g.np - 1] : 0.0;
-    const double2* cp = reinterpret_cast<const double2*>(colpts);
-    double2* dst = reinterpret_cast<double2*>(tile + r);
-#pragma unroll kCovUnroll
-    for (int c = c0; c < c0 + cw; ++c) {
-      const double2 pc = cp[c];
-      const double ax = x0.x - pc.x, ay = x0.y - pc.y;
-      const double bx = x1.x - pc.x, by = x1.y - pc.y;
-      double2 v;
-      v.x = cov_fast<KIND>(fma(ax, ax, ay * ay), sc, tab);
-      v.y = cov_fast<KIND>(fma(bx, bx, by * by), sc, tab);
-      if (I == J) {  // rows r, r+1 of a diagonal tile: lower part, nugget where i == j
-        v.x = c > r ? 0.0 : (c == r ? v.x + tau2 : v.x);
-        v.y = c > r + 1 ? 0.0 : (c == r + 1 ? v.y + tau2 : v.y);
-      }
-      __stcs(dst + (int64_t)c * (b / 2), v);
+  if (fast) {
+    const bool padded = i0 + b > n || j0 + b > n;
+    if (I == J) {
+      if (padded) cov_tile_fast<KIND, true, true>(g, X, n, b, i0, j0, colpts, tab, tile);
+      else cov_tile_fast<KIND, true, false>(g, X, n, b, i0, j0, colpts, tab, tile);
+    } else {
+      if (padded) cov_tile_fast<KIND, false, true>(g, X, n, b, i0, j0, colpts, tab, tile);
+      else cov_tile_fast<KIND, false, false>(g, X, n, b, i0, j0, colpts, tab, tile);
     }
     return;
   }
