@@ -184,6 +184,11 @@ struct GemmProblem {
   // zeroed int: the first CTA to take a ticket is the look-ahead CTA
   // (null: launch_gemm provides one)
   int* role_ticket;
+  // GEMM_CHOL_TRAIL fused TRSM by substitution (tiles >= 256, chain-bound
+  // steps): no tile inverse; each slab task solves its 128 rows column block
+  // by column block as the look-ahead POTRF publishes them (potrf_progress)
+  int trsm_subst;
+  int* potrf_progress;
   // GEMM_CHOL_TRAIL: live rows of the triangle (rows >= n_live are identity
   // padding); blocks and TRSM slabs wholly in the padding are skipped (0: none)
   int64_t n_live;

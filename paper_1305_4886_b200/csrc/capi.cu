@@ -246,8 +246,8 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   const size_t dinv_bytes = (size_t)nbk * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
-  // published, [T+1] look-ahead ticket, [stride-2, stride) the 64-bit task
-  // counter of the step's launch
+  // published, [T+1] look-ahead ticket, [T+2] POTRF progress (substitution
+  // TRSM), [stride-2, stride) the 64-bit task counter of the step's launch
   const int stride = (T + 4 + 1) & ~1;
   if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
@@ -262,6 +262,11 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     return !(e && atoi(e) == 0);
   }();
   const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);  // any block shape with BM, BN >= 64
+  // chain-bound steps at tiles >= 256: fused TRSM by substitution (BGP_TRSM_SUBST=0: inverse + GEMM)
+  static const bool trsm_subst = [] {
+    const char* e = getenv("BGP_TRSM_SUBST");
+    return !(e && atoi(e) == 0);
+  }();
   if (trsm_par) {
     if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
     cudaError_t e = cudaMemsetAsync(ctx->d_pass, 0, (size_t)T * pass_stride * sizeof(int), s);
@@ -344,7 +349,12 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
         // waiting on passes to their right are idle anyway, while in large
         // steps the waits would cost update throughput
         const int k_par = b <= 128 ? 48 : (b <= 256 ? 26 : (b <= 384 ? 22 : 18));
-        if (trsm_par && T - J - 1 <= k_par) {
+        if (trsm_subst && b >= 256 && T - J - 1 <= k_par) {
+          // tiles >= 256 (factored in place): the panel solve by
+          // substitution follows the POTRF block by block (no tile inverse)
+          p.trsm_subst = 1;
+          p.potrf_progress = gate + T + 2;
+        } else if (trsm_par && T - J - 1 <= k_par) {
           p.trsm_par = 1;
           p.pass_done = ctx->d_pass + (int64_t)J * pass_stride;
         }

@@ -92,6 +92,7 @@ struct Item {
   int slab, pass;            // trsm_par TRSM pass: slab index, pass (0 = rightmost); else slab = -1
   bool valid;
   bool pad;                  // skipped: every row lies in the identity padding (its gate still counts)
+  bool subst;                // fused TRSM slab solved by substitution (no TMA stages)
 };
 
 __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p) {
@@ -205,6 +206,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   it.nkt = 1;
   it.valid = true;
   it.pad = false;
+  it.subst = false;
   it.lower = 0;
   it.bTriRow = -1;
   it.kstages = 0;
@@ -228,6 +230,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
                            : p.mode == GEMM_RECT_TRAIL                       ? (int64_t)(p.J + 1) * p.Tm
                                                                              : tri_index(p.J + 2, p.J + 1, p.T);
     trsm_block(it, p, idx, pass, panel0);
+    it.subst = p.mode == GEMM_CHOL_TRAIL && p.trsm_subst;
     // Cholesky sweep: slabs of the last tile row that lie wholly in the
     // padding hold zeros and solve to zeros -- skipped
     if (p.mode == GEMM_CHOL_TRAIL && p.n_live > 0 &&
@@ -307,7 +310,8 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
-  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) && !gemm_par_passes(p))
+  return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) && !gemm_par_passes(p) &&
+          !(p.mode == GEMM_CHOL_TRAIL && p.trsm_subst))
              ? p.b / BN
              : 1;
 }
@@ -412,7 +416,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       }
       const int g0 = p.mode == GEMM_RECT_TRAIL ? 0 : 1;  // Cholesky gate 0 is the diagonal tile
       if (!wait_count(p.col_gate + g0 + tile, p.tile_need, info) ||
-          (p.linv_flag && !wait_count(p.linv_flag, p.linv_need, info)))
+          (p.linv_flag && !p.trsm_subst && !wait_count(p.linv_flag, p.linv_need, info)))
         break;
       fence_proxy_async_global();
     }
@@ -422,6 +426,28 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       if (!it.valid) {
         // a padding block counts toward its tile's gate as if it had retired
         if (it.pad && it.gate >= 0) atomicAdd(p.col_gate + it.gate, GROUP_WARPS);
+        continue;
+      }
+      if (it.subst) {
+        // substitution slab: no operand stages, the consumers read the tile,
+        // the factor and Dinv themselves as the POTRF publishes them
+        mbar_wait(&gs.empty[stage], phase ^ 1);
+        BlockSlot& sl = gs.slot[stage];
+        sl.valid = 1;
+        sl.cTile = it.cTile;
+        sl.mrow0 = it.mrow0;
+        sl.nrow0 = 0;
+        sl.nk = 0;
+        sl.lower = sl.store = 0;
+        sl.gate = -1;
+        sl.slab = -1;
+        sl.pass = 0;
+        sl.pad[0] = 1;
+        mbar_arrive(&gs.full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
         continue;
       }
       const CUtensorMap* tb = it.bLinv ? tmL : tmB;
@@ -441,6 +467,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
           sl.gate = it.gate;
           sl.slab = it.slab;
           sl.pass = it.pass;
+          sl.pad[0] = 0;
         }
         mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
         const int kt = kc / kc_per_tile;
@@ -573,6 +600,88 @@ __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ]
   }
 }
 
+// Panel solve by substitution for one warp: rows r0 .. r0+31 of the panel
+// tile X (in place), X_k = (A_k - sum_{j<k} X_j L_kj^T) Dinv_k^T over the
+// 32-column blocks k of the diagonal tile L = p.potrf_tile, each block as
+// soon as the look-ahead POTRF has published it (p.potrf_progress > k), so
+// the solve finishes about one block after the factorization instead of
+// after a full tile inverse (bg/distla/kernels.py:163-164).  Fragments:
+// DMMA 8x8x4, acc[tr][tc][e] = C(tr*8 + q, tc*8 + 2 s4 + e).
+__device__ __noinline__ void trsm_subst_rows(int b, const double* __restrict__ Ld, const double* __restrict__ Dv,
+                                             const int* progress, double* __restrict__ X, int r0, int lane,
+                                             unsigned long long* info) {
+  const int nbk = b / 32;
+  const int q = lane >> 2, s4 = lane & 3;
+  double* Xr = X + r0;
+  for (int k = 0; k < nbk; ++k) {
+    bool ok = true;
+    if (lane == 0) ok = wait_count(progress, k + 1, info);
+    if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) return;  // factorization failed
+    __syncwarp();  // lane 0's acquire orders every lane's reads below (all from L2)
+    double acc[4][4][2];
+#pragma unroll
+    for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+      for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[tr][tc][e] = __ldcg(Xr + (int64_t)(32 * k + tc * 8 + 2 * s4 + e) * b + tr * 8 + q);
+    for (int j = 0; j < k; ++j) {  // acc -= X_j L_kj^T
+#pragma unroll
+      for (int kh = 0; kh < 2; ++kh) {
+        double av[4][4], bv[4][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int kc = 32 * j + 16 * kh + 4 * kk + s4;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            av[kk][t] = -__ldcg(Xr + (int64_t)kc * b + t * 8 + q);
+            bv[kk][t] = __ldcg(Ld + (int64_t)kc * b + 32 * k + t * 8 + q);
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+            for (int tc = 0; tc < 4; ++tc) dmma884(acc[tr][tc][0], acc[tr][tc][1], av[kk][tr], bv[kk][tc]);
+      }
+    }
+    // X_k = acc Dinv_k^T: acc to A fragments within each quad (A(row, c) for
+    // c = 4 kk + s4 sits in lane ((kk & 1) * 2 + (s4 >> 1)) of the quad,
+    // element s4 & 1 of column tile kk >> 1)
+    double out[4][4][2];
+#pragma unroll
+    for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+      for (int tc = 0; tc < 4; ++tc) out[tr][tc][0] = out[tr][tc][1] = 0.0;
+    const double* Dk = Dv + (int64_t)k * 1024;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int src = (lane & ~3) | ((kk & 1) * 2 + (s4 >> 1));
+      double af[4], bd[4];
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr) {
+        const double v0 = __shfl_sync(0xffffffffu, acc[tr][kk >> 1][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, acc[tr][kk >> 1][1], src);
+        af[tr] = (s4 & 1) ? v1 : v0;
+      }
+#pragma unroll
+      for (int tc = 0; tc < 4; ++tc) bd[tc] = __ldcg(Dk + (4 * kk + s4) * 32 + tc * 8 + q);  // Dinv_k^T
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc) dmma884(out[tr][tc][0], out[tr][tc][1], af[tr], bd[tc]);
+    }
+#pragma unroll
+    for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+      for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Xr[(int64_t)(32 * k + tc * 8 + 2 * s4 + e) * b + tr * 8 + q] = out[tr][tc][e];
+    __syncwarp();  // X_k visible to the warp's lanes before the next blocks read it
+  }
+}
+
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p,
                                               uint64_t* stagger, const PushMaps* pm,
@@ -625,6 +734,23 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
     mbar_wait(&gs.full[stage], phase);  // first stage of the next block (or the sentinel)
     const BlockSlot it = gs.slot[stage];
     if (!it.valid) break;
+    if (it.pad[0]) {  // fused TRSM slab by substitution: 32 rows per warp
+      release_held();
+      if (stagger_arrive) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stagger);
+        stagger_arrive = false;
+      }
+      trsm_subst_rows(p.b, p.potrf_tile, p.dinv, p.potrf_progress, p.cbase + (int64_t)it.cTile * p.b * p.b,
+                      it.mrow0 + 32 * gwarp, lane, info);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gs.empty[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      continue;
+    }
     const int nk = it.nk;
     double acc[MI][NJ][2];
 #pragma unroll
@@ -817,8 +943,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
         named_bar_sync(2, 256);
         const bool la_ok = s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
-                                                        p.trsm_next ? p.linv : nullptr, psm, ctid, 2);
-        if (la_ok && p.trsm_next) {
+                                                        (p.trsm_next && !p.trsm_subst) ? p.linv : nullptr,
+                                                        psm, ctid, 2, p.trsm_subst ? p.potrf_progress : nullptr);
+        if (la_ok && p.trsm_next && !p.trsm_subst) {
           __threadfence();
           named_bar_sync(2, 256);
           if (ctid == 0) atomicAdd(p.linv_flag, p.b / 32);

@@ -278,9 +278,21 @@ __device__ __forceinline__ void linv_row_partial(const double* __restrict__ L, b
 // spreads the work more evenly but its read-modify-write of the partial
 // sums measured slower.)
 // l_smem: A is a shared-memory copy (see tile_potrf_inv_device).
+// progress (A in global memory only): after diagonal block k's factor, its
+// inverse Dinv_k and L's row block k (all columns < k) are final, the
+// counter is raised to k + 1 (release; every thread fences first) -- the
+// in-launch substitution panel solve (gemm.cu) consumes the factor that way
+// while the factorization is still running.
+__device__ __forceinline__ void potrf_publish(int* progress, int v, int tid, int bar) {
+  __threadfence();
+  named_bar_sync(bar, POTRF_THREADS);
+  if (tid == 0) st_release_gpu(progress, v);
+}
+
 static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, int b, int64_t row0, double* __restrict__ dinv,
                                   unsigned long long* __restrict__ info, double* sm, int tid, int bar,
-                                  double* __restrict__ Linv = nullptr, bool l_smem = false) {
+                                  double* __restrict__ Linv = nullptr, bool l_smem = false,
+                                  int* progress = nullptr) {
   double* D = sm;                // 32 x 33
   double* Dinv_s = D + NB * 33;  // 32 x 33
   double* P = Dinv_s + NB * 33;  // (b - 32) x PLD
@@ -311,6 +323,7 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
   }
   named_bar_sync(bar, POTRF_THREADS);
   if (*s_fail) return false;
+  if (progress) potrf_publish(progress, 1, tid, bar);
   for (int kb = 0; kb + 1 < nbk; ++kb) {
     const int c0 = kb * NB;
     const int rest = b - c0 - NB;
@@ -397,6 +410,7 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
     __threadfence_block();
     named_bar_sync(bar, POTRF_THREADS);
     if (*s_fail) return false;
+    if (progress) potrf_publish(progress, kb + 2, tid, bar);
   }
   if (Linv) {  // the last row block of the inverse
     linv_row_apply(dinv, Linv, b, nbk - 1, warp, POTRF_THREADS / 32, lane);
@@ -502,9 +516,10 @@ constexpr int SMEM_TILE = 128;
 static __device__ __noinline__ bool tile_potrf_inv_device(double* __restrict__ A, int b, int64_t row0,
                                                           double* __restrict__ dinv,
                                                           unsigned long long* __restrict__ info,
-                                                          double* __restrict__ Linv, double* sm, int tid, int bar) {
+                                                          double* __restrict__ Linv, double* sm, int tid, int bar,
+                                                          int* progress = nullptr) {
   static_assert(POTRF_THREADS == TINV_THREADS, "one thread set");
-  if (b > SMEM_TILE) return tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar, Linv, false);
+  if (b > SMEM_TILE) return tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar, Linv, false, progress);
   double* T = sm;
   double* scratch = sm + (size_t)b * b;
   const int n2 = b * b / 2;

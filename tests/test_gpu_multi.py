@@ -262,3 +262,50 @@ def test_dist_sweep_steps_in_one_process(cluster_factory, tile, nt, push):
     for k, (I, J) in enumerate(td.tiles):
         L[I * tile:(I + 1) * tile, J * tile:(J + 1) * tile] = local[k].cpu().numpy().T
     assert relerr(L[:n, :n], np.linalg.cholesky(A)) <= 1e-12
+
+
+def _tail_worker(rank, world, port, q, n):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank), LOCAL_RANK="0")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import blockgp_oracle as orc
+        from paper_1305_4886_b200.gp import KrigeProblem, builtin_spec
+        from paper_1305_4886_b200 import spawn
+        kern, X, theta, extra, z = orc.config_inputs(4, n=n)
+        cl = spawn(world, tile=256, device=0)
+        prob = KrigeProblem(cl, "t", builtin_spec(kern, X, **extra), z, theta)
+        q.put((rank, prob.log_density()))
+        cl.shutdown()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_sweep_with_gathered_tail_two_ranks():
+    """2 ranks on one GPU at a size where the sweep's last 24 tile rows of
+    256 are gathered and finished on every rank (parallel.factor_tail): the
+    log-density equals the single-GPU path's."""
+    import torch.multiprocessing as mp
+    from oracle import blockgp_oracle as orc
+    from paper_1305_4886_b200 import spawn
+    from paper_1305_4886_b200.gp import KrigeProblem, builtin_spec
+    n = 52 * 256 - 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tail_worker, args=(r, 2, port, q, n)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    kern, X, theta, extra, z = orc.config_inputs(4, n=n)
+    cl = spawn(1, tile=256)
+    try:
+        want = KrigeProblem(cl, "t", builtin_spec(kern, X, **extra), z, theta).log_density()
+    finally:
+        cl.shutdown()
+    assert out[0] == out[1]
+    assert abs(out[0] - want) <= 1e-10 * abs(want)
