@@ -248,7 +248,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
   // published, [T+1] look-ahead ticket, [T+2] POTRF progress (substitution
   // TRSM), [stride-2, stride) the 64-bit task counter of the step's launch
-  const int stride = (T + 4 + 1) & ~1;
+  const int stride = (T + 6 + 1) & ~1;  // [T, T+3] flags, then the 64-bit queue (even offset)
   if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_linv, &ctx->linv_cap, (size_t)b * b * sizeof(double)))) return rc;
   {
