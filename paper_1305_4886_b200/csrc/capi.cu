@@ -931,7 +931,7 @@ int bgp_dist_begin(bgp_ctx_t ctx, int T, int tile, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int b = tile;
   int rc;
-  const int stride = (T + 4 + 1) & ~1;
+  const int stride = (T + 6 + 1) & ~1;  // [T, T+3] flags, then the 64-bit queue
   const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);
   if ((rc = ensure(ctx, (void**)&ctx->d_gate, &ctx->gate_cap, (size_t)T * stride * sizeof(int)))) return rc;
   if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
@@ -966,7 +966,7 @@ int bgp_dist_step(bgp_ctx_t ctx, int J, double* local, int64_t nlocal, const dou
     return BGP_E_ARG;
   if (count == 0 && !diag) return BGP_OK;
   const int b = tile;
-  const int stride = (T + 4 + 1) & ~1;
+  const int stride = (T + 6 + 1) & ~1;  // [T, T+3] flags, then the 64-bit queue
   const int64_t pass_stride = (int64_t)T * (b / 64) * (b / 64);
   int* gate = ctx->d_gate + (int64_t)J * stride;
   int tile_need, diag_need, groups_per_cta;
@@ -999,9 +999,14 @@ int bgp_dist_step(bgp_ctx_t ctx, int J, double* local, int64_t nlocal, const dou
     p.trsm_count = trsm_count;
     p.panel0 = trsm_first;
     p.trsm_tail = 6 * groups_per_cta * ctx->num_sms;
-    if (trsm_par && trsm_count > 0) {
-      p.trsm_par = 1;
-      p.pass_done = ctx->d_pass + (int64_t)J * pass_stride;
+    if (trsm_par && trsm_count > 0) {  // a chain-bound step
+      if (b >= 256) {  // substitution behind the POTRF (progress at [T+2])
+        p.trsm_subst = 1;
+        p.potrf_progress = gate + T + 2;
+      } else {
+        p.trsm_par = 1;
+        p.pass_done = ctx->d_pass + (int64_t)J * pass_stride;
+      }
     }
     if (ndst > 0 && trsm_count > 0) {
       p.npush = ndst;

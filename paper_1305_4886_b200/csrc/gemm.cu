@@ -230,7 +230,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
                            : p.mode == GEMM_RECT_TRAIL                       ? (int64_t)(p.J + 1) * p.Tm
                                                                              : tri_index(p.J + 2, p.J + 1, p.T);
     trsm_block(it, p, idx, pass, panel0);
-    it.subst = p.mode == GEMM_CHOL_TRAIL && p.trsm_subst;
+    it.subst = (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST) && p.trsm_subst;
     // Cholesky sweep: slabs of the last tile row that lie wholly in the
     // padding hold zeros and solve to zeros -- skipped
     if (p.mode == GEMM_CHOL_TRAIL && p.n_live > 0 &&
@@ -311,7 +311,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
   return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) && !gemm_par_passes(p) &&
-          !(p.mode == GEMM_CHOL_TRAIL && p.trsm_subst))
+          !((p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST) && p.trsm_subst))
              ? p.b / BN
              : 1;
 }
@@ -347,6 +347,7 @@ __device__ __forceinline__ uint32_t lane_off(int p, int t, int q, int s4) {
 // tensor maps of the panel push destinations (GEMM_TRSM_PANEL, npush > 0)
 struct PushMaps {
   CUtensorMap map[BGP_MAX_PUSH];
+  double* ptr[BGP_MAX_PUSH];  // the same destinations as raw pointers (substitution panel solve)
 };
 
 // What the consumers need of a block, decoded once by the producer and
@@ -607,9 +608,13 @@ __device__ __forceinline__ void stage_halves(Frag (&f)[2], double (&acc)[MI][NJ]
 // the solve finishes about one block after the factorization instead of
 // after a full tile inverse (bg/distla/kernels.py:163-164).  Fragments:
 // DMMA 8x8x4, acc[tr][tc][e] = C(tr*8 + q, tc*8 + 2 s4 + e).
+// With npush > 0 every solved block is also stored into tile `slot` of each
+// destination panel buffer (the distributed sweep's exchange, plain stores
+// to peer memory over NVLink).
 __device__ __noinline__ void trsm_subst_rows(int b, const double* __restrict__ Ld, const double* __restrict__ Dv,
                                              const int* progress, double* __restrict__ X, int r0, int lane,
-                                             unsigned long long* info) {
+                                             unsigned long long* info, const PushMaps* pm, int npush,
+                                             int64_t slot) {
   const int nbk = b / 32;
   const int q = lane >> 2, s4 = lane & 3;
   double* Xr = X + r0;
@@ -678,6 +683,15 @@ __device__ __noinline__ void trsm_subst_rows(int b, const double* __restrict__ L
       for (int tc = 0; tc < 4; ++tc)
 #pragma unroll
         for (int e = 0; e < 2; ++e) Xr[(int64_t)(32 * k + tc * 8 + 2 * s4 + e) * b + tr * 8 + q] = out[tr][tc][e];
+    for (int d = 0; d < npush; ++d) {
+      double* Pr = pm->ptr[d] + slot * b * b + r0;
+#pragma unroll
+      for (int tr = 0; tr < 4; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < 4; ++tc)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) Pr[(int64_t)(32 * k + tc * 8 + 2 * s4 + e) * b + tr * 8 + q] = out[tr][tc][e];
+    }
     __syncwarp();  // X_k visible to the warp's lanes before the next blocks read it
   }
 }
@@ -742,7 +756,7 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         stagger_arrive = false;
       }
       trsm_subst_rows(p.b, p.potrf_tile, p.dinv, p.potrf_progress, p.cbase + (int64_t)it.cTile * p.b * p.b,
-                      it.mrow0 + 32 * gwarp, lane, info);
+                      it.mrow0 + 32 * gwarp, lane, info, pm, p.npush, (int64_t)it.cTile - p.panel0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&gs.empty[stage]);
       if (++stage == STAGES) {
@@ -1018,6 +1032,7 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
     return set_err(ctx, "gemm: bad push destinations", cudaErrorInvalidValue);
   for (int d = 0; d < p.npush; ++d)
     if ((rc = make_tile_map(ctx, &pm.map[d], p.push_dst[d], p.b, p.push_tiles, 16, WN, true)) != BGP_OK) return rc;
+  for (int d = 0; d < p.npush; ++d) pm.ptr[d] = p.push_dst[d];
   prepare();
   int64_t slots = (p.grid_limit > 0 && p.grid_limit < ctx->num_sms) ? p.grid_limit : ctx->num_sms;
   if (ctx->grid_cap > 0 && ctx->grid_cap < slots) slots = ctx->grid_cap;
