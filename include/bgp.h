@@ -111,10 +111,11 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
  * row of the first non-positive pivot (LAPACK potrf convention); the caller
  * maps it to NotPositiveDefinite(block) with its layout (kernels.py:146-148).
  * The schedule has a one-panel look-ahead inside one launch per step: the
- * launch's last CTA factors the next panel's diagonal tile (building its
- * inverse during the factorization) once that tile's update blocks have
- * retired, and the next panel's solve runs as gated tasks of the same
- * launch.  Every wait is inside the launch, so the
+ * first CTA to take the look-ahead ticket factors the next panel's
+ * diagonal tile (building its inverse during the factorization, or
+ * publishing its progress per 32 columns for a substitution solve) once that
+ * tile's update blocks have retired, and the next panel's solve runs as
+ * gated tasks of the same launch.  Every wait is inside the launch, so the
  * schedule also holds when kernels are serialised (Nsight Compute).
  * BGP_LOOKAHEAD=0 in the environment runs POTRF, inverse, solve and update
  * as separate launches one after another on `stream` (diagnostics). */

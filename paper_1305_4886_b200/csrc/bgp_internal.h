@@ -148,7 +148,7 @@ struct GemmProblem {
   int* linv_flag;
   int linv_need;
   int trsm_tail;       // update blocks queued after the fused TRSM tasks (tail filler)
-  // look-ahead inside the launch: the last CTA first factors tile potrf_tile
+  // look-ahead inside the launch: the first CTA to take role_ticket factors tile potrf_tile
   // (panel J+1's diagonal, once col_gate[0] reaches diag_need) into dinv, and
   // with trsm_next its inverse into linv (published through linv_flag), then
   // joins the queue

@@ -207,7 +207,7 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen, const doubl
 // queue holds the update blocks (tile column J+1 first), the in-place TRSM of
 // panel J+1, and a tail of update blocks.  Warps that reduce into a tile of
 // column J+1 bump that tile's counter once their bulk reductions retired.
-// The launch's last CTA first waits for the diagonal tile's counter, factors
+// The first CTA to take the role ticket waits for the diagonal tile's counter, factors
 // tile (J+1, J+1) and inverts it on its ring memory, publishes the inverse,
 // and then joins the queue; the TRSM tasks wait for their tile's counter and
 // the inverse.  So the latency-bound POTRF and the panel TRSM both run under
@@ -331,7 +331,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     const bool next = K < J_stop;  // panel K is factored here
     if (la_mode == 1) {
       if (next) {
-        // POTRF(K) (+ inverse) by the launch's last CTA, the TRSM of panel K
+        // POTRF(K) (+ inverse) by the CTA holding the role ticket, the TRSM of panel K
         // as gated tasks of the same launch
         p.col_gate = gate;
         p.trsm_next = (K + 1 < T);
@@ -349,9 +349,9 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
         // waiting on passes to their right are idle anyway, while in large
         // steps the waits would cost update throughput
         const int k_par = b <= 128 ? 48 : (b <= 256 ? 26 : (b <= 384 ? 22 : 18));
-        if (trsm_subst && b >= 256 && T - J - 1 <= k_par) {
-          // tiles >= 256 (factored in place): the panel solve by
-          // substitution follows the POTRF block by block (no tile inverse)
+        if (trsm_subst && T - J - 1 <= k_par) {
+          // the panel solve by substitution follows the POTRF block by block
+          // (no tile inverse; 128 tiles are then factored in place too)
           p.trsm_subst = 1;
           p.potrf_progress = gate + T + 2;
         } else if (trsm_par && T - J - 1 <= k_par) {

@@ -519,7 +519,9 @@ static __device__ __noinline__ bool tile_potrf_inv_device(double* __restrict__ A
                                                           double* __restrict__ Linv, double* sm, int tid, int bar,
                                                           int* progress = nullptr) {
   static_assert(POTRF_THREADS == TINV_THREADS, "one thread set");
-  if (b > SMEM_TILE) return tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar, Linv, false, progress);
+  // a published factor must be in global memory: with progress the tile is
+  // factored in place whatever its size
+  if (b > SMEM_TILE || progress) return tile_potrf_device(A, b, row0, dinv, info, sm, tid, bar, Linv, false, progress);
   double* T = sm;
   double* scratch = sm + (size_t)b * b;
   const int n2 = b * b / 2;
