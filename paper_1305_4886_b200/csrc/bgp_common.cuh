@@ -187,6 +187,11 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// arrive on a named barrier without waiting (the producer side of a
+// producer / consumer hand-off inside a CTA)
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).  sm_100a lowers
 // this to DMMA.8x8x4.  Lane l holds A[l/4][l%4], B[l%4][l/4],

@@ -9,6 +9,21 @@
 namespace bgp {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// BGP_POTRF_TRACE (probe builds only, tools/probes/potrf_trace.cu): lane 0 of
+// warps 0 and 1 stamp clock64() at the phase boundaries of tile_potrf_device
+#ifdef BGP_POTRF_TRACE
+__device__ long long g_ptrace[2][1024];
+#define PTRACE()                                                                \
+  do {                                                                          \
+    if (lane == 0 && warp < 2 && pt_n < 1024) g_ptrace[warp][pt_n] = clock64(); \
+    ++pt_n;                                                                     \
+  } while (0)
+#else
+#define PTRACE() \
+  do {           \
+  } while (0)
+#endif
 constexpr int NB = 32;        // sub-panel width
 constexpr int PLD = 36;       // smem leading dimension of the panel copy (conflict-free DMMA frags)
 constexpr int POTRF_THREADS = 256;
@@ -302,6 +317,10 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) *s_fail = 0;
   const int nbk = b / NB;
+#ifdef BGP_POTRF_TRACE
+  int pt_n = 0;
+#endif
+  PTRACE();
   if (Linv) {  // strictly upper blocks of the inverse are zero: warp per column
     for (int c = warp; c < b; c += POTRF_THREADS / 32) {
       double2* colp = reinterpret_cast<double2*>(Linv + (int64_t)c * b);
@@ -321,10 +340,12 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
       warp_trinv32(D, rdiag, Dinv_s, dinv, lane);
     }
   }
+  PTRACE();
   named_bar_sync(bar, POTRF_THREADS);
   if (*s_fail) return false;
   if (progress) potrf_publish(progress, 1, tid, bar);
   for (int kb = 0; kb + 1 < nbk; ++kb) {
+    PTRACE();  // 2 + 6 kb
     const int c0 = kb * NB;
     const int rest = b - c0 - NB;
     // (A) sub-panel X = A[c0+32:, c0:c0+32] Dinv_k^T (in place + smem copy),
@@ -373,7 +394,9 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
           }
     }
     if (Linv) __threadfence_block();  // inverse row kb before step kb's partial sums read it
+    PTRACE();  // 3 + 6 kb: sub-panel phase done
     named_bar_sync(bar, POTRF_THREADS);
+    PTRACE();  // 4 + 6 kb
     // (B) trailing update in 32x32 blocks; block (0, 0) is diagonal block k+1
     const int nb32 = rest / 32;
     const int nblk = nb32 * (nb32 + 1) / 2;
@@ -382,7 +405,9 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
       trail_block32(A, b, base_rc, P, 0, 0, lane);
       __syncwarp();
       __threadfence_block();
+      PTRACE();  // 5 + 6 kb (warp 0): diagonal block updated
       const unsigned fm = warp_potrf32(A, b, base_rc, D, rdiag, col, lane);
+      PTRACE();  // 6 + 6 kb (warp 0): factored
       if (fm) {
         if (lane == 0) {
           if (info) set_info(info, row0 + base_rc + __ffs(fm));
@@ -406,7 +431,10 @@ static __device__ __noinline__ bool tile_potrf_device(double* __restrict__ A, in
         while (bi * (bi + 1) / 2 > t) --bi;
         trail_block32(A, b, base_rc, P, bi, t - bi * (bi + 1) / 2, lane);
       }
+      PTRACE();  // 5 + 6 kb (warp 1): trailing blocks done
+      PTRACE();
     }
+    PTRACE();  // 7 + 6 kb: warp 0 inverted / warp 1 done
     __threadfence_block();
     named_bar_sync(bar, POTRF_THREADS);
     if (*s_fail) return false;
