@@ -50,16 +50,21 @@ CUBLAS_DGEMM = 35.8
 REF_SUB_BLOCKS = 20  # reference sampler: sub-evaluation of 20 reference blocks (19,800 points)
 
 
+# the committed ncu --set full capture of one C4 trailing-update launch
+# (k = 111 tiles of 512) that the roofline's `traffic` comes from
+GEMM_NCU_CAPTURE = "profiles/r02l2_ncu_gemm_full.txt"
+
+
 def gemm_traffic():
     """DRAM bytes (read + write) of one trailing-update launch from the
     committed ncu --set full capture (profiles/*_ncu_gemm_full.txt), with the
     algorithmic bytes of the same launch; None when no capture is committed."""
-    import glob
     import re
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_gemm_full.txt")))
-    if not files:
+    path = os.path.join(ROOT, GEMM_NCU_CAPTURE)
+    if not os.path.exists(path):
         return None, None
-    txt = open(files[-1]).read()
+    files = [path]
+    txt = open(path).read()
     m = re.search(r"traffic \(read\+write\)\s+([0-9.e+]+) B", txt)
     f = re.search(r"algorithmic flops\s+([0-9.e+]+)", txt)
     if not m or not f:
@@ -69,7 +74,7 @@ def gemm_traffic():
     algo = 8.0 * b * b * (k * (k + 1) + k)  # C tiles read + written once, panel read once
     return float(m.group(1)), {"file": os.path.relpath(files[-1], ROOT), "launch_trailing_tiles": k,
                                "algorithmic_bytes": algo,
-                               "note": "one captured step; the k-tile panel exceeds L2 and is re-read"}
+                               "note": "one captured step (k-tile panel read once per L2 super-column)"}
 
 
 def load_c4():

@@ -197,6 +197,46 @@ __device__ __forceinline__ void trsm_block(Item& it, const GemmProblem& p, int64
   it.bLinv = 1;
 }
 
+// Order of the trailing triangle's k(k+1)/2 tiles in a Cholesky update
+// launch: tile column J+1 first (the next panel: its blocks gate the
+// look-ahead POTRF and solve), then super-columns of sw tile columns, each
+// swept top to bottom, row by row.  A super-column's sw panel tiles (the B
+// operands) stay in L2 while each row's panel tile (the A operand) is read
+// from HBM once per super-column instead of once per tile column: the k-tile
+// panel (233 MB at C4's first steps) exceeds L2, and a column-by-column sweep
+// re-read it k/2 times (1.5x the algorithmic bytes per launch, round 1).
+// The permutation changes no arithmetic: every C tile still receives one
+// update per step.
+__device__ __forceinline__ void trail_order(int64_t t, int k, int sw, int& rr, int& cc) {
+  if (t < k) {
+    rr = (int)t;
+    cc = 0;
+    return;
+  }
+  t -= k;
+  for (int c0 = 1; c0 < k; c0 += sw) {
+    const int w = min(sw, k - c0);
+    const int64_t tri = (int64_t)w * (w + 1) / 2;  // rows c0 .. c0+w-1: row c0+i holds i+1 tiles
+    const int64_t n = tri + (int64_t)(k - c0 - w) * w;
+    if (t < n) {
+      if (t < tri) {
+        int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+        while ((int64_t)i * (i + 1) / 2 > t) --i;
+        rr = c0 + i;
+        cc = c0 + (int)(t - (int64_t)i * (i + 1) / 2);
+      } else {
+        const int64_t u = t - tri;
+        rr = c0 + w + (int)(u / w);
+        cc = c0 + (int)(u % w);
+      }
+      return;
+    }
+    t -= n;
+  }
+  rr = cc = 0;  // unreachable for t < k(k+1)/2
+}
+
 // Block `pass` of task `task`.
 __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, int pass) {
   const int nbn = p.b / BN;
@@ -247,7 +287,9 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
       int rr, cc;
-      tri_decode(t, p.T - p.J - 1, rr, cc);
+      // super-column width: ~16 MB of panel tiles, 8 .. 64 tiles
+      const int sw = max(8, min(64, (int)((16ll << 20) / ((int64_t)p.b * p.b * 8))));
+      trail_order(t, p.T - p.J - 1, sw, rr, cc);
       const int R = p.J + 1 + rr, C = p.J + 1 + cc;
       it.cTile = tri_index(R, C, p.T);
       it.aTile0 = tri_index(R, p.J, p.T);
