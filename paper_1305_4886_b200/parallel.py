@@ -158,7 +158,13 @@ class TileDist:
         rows = []
         if len(t):
             R, C = t[:, 0].astype(np.int64), t[:, 1].astype(np.int64)
-            rows.append(np.stack([np.arange(first, first + len(t)), slot[R], slot[C], (R == C)], axis=1))
+            # L2 super-columns (as the single-GPU update, gemm.cu
+            # trail_order): ~16 MB of B-operand panel tiles per group of
+            # local columns, swept row by row, so each A-operand panel tile
+            # is read from HBM once per group instead of once per column
+            sw = max(8, min(64, (16 << 20) // (self.b * self.b * 8)))
+            order = np.lexsort((C, R, (C // self.grid.shape[1]) // sw))
+            rows.append(np.stack([np.arange(first, first + len(t)), slot[R], slot[C], (R == C)], axis=1)[order])
         sh = [(self.shadow_local[K], slot[K], slot[K], 1) for K in self.shadows if K > J]
         if sh:
             rows.append(np.array(sh, dtype=np.int64))
