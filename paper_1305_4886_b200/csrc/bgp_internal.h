@@ -44,6 +44,8 @@ struct Ctx {
   size_t linv_cap = 0;
   int* d_pass = nullptr;  // per-step pass counters of the parallel fused TRSM
   size_t pass_cap = 0;
+  int* d_multi = nullptr;  // counters of the multi-step tail launch (tiles, solves, progress, queue)
+  size_t multi_cap = 0;
   double* d_linv_all = nullptr;  // inverses of every diagonal tile (kriging solve)
   size_t linv_all_cap = 0;
   // per-launch task counters (+ look-ahead tickets) of GEMM launches that do
@@ -195,6 +197,22 @@ struct GemmProblem {
   // tile counts behind the A / B / C tensor maps (set by launch_gemm; the
   // checked build asserts every tile index against them)
   int64_t nA, nB, nC;
+  // GEMM_CHOL_TRAIL over nsteps > 1 consecutive steps J .. J+nsteps-1 in ONE
+  // launch (the chain-bound tail, substitution solve): the steps' task lists
+  // are queued one after another and ordered by counters instead of launch
+  // boundaries.  tile_cnt[t] counts the retired warp-blocks of trailing tile
+  // t (packed index minus cnt_base = tri_index(J+1, J+1, T); col_gate points
+  // at it), solved[t] the warps that finished solving panel tile t by
+  // substitution (solved_need per tile).  An update block of step s > J
+  // waits until its two panel-s tiles are solved; the solve of tile
+  // (R, s+1) waits for (s+1-J) steps of updates into it; the role CTA factors
+  // (s+1, s+1) after (s+1-J) steps of updates, into dinv + (s-J) * b * 32
+  // with progress counter potrf_progress[s-J].
+  int nsteps;
+  int* tile_cnt;
+  int* solved;
+  int solved_need;
+  int64_t cnt_base;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

@@ -179,6 +179,7 @@ int bgp_finalize(bgp_ctx_t ctx) {
   if (ctx->d_linv) cudaFree(ctx->d_linv);
   if (ctx->d_linv_all) cudaFree(ctx->d_linv_all);
   if (ctx->d_pass) cudaFree(ctx->d_pass);
+  if (ctx->d_multi) cudaFree(ctx->d_multi);
   if (ctx->d_queue_ring) cudaFree(ctx->d_queue_ring);
   for (int l = 0; l < 2; ++l)
     if (ctx->d_tail[l]) cudaFree(ctx->d_tail[l]);
@@ -243,7 +244,11 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   const int T = (int)((n + b - 1) / b);
   const int nbk = b / 32;
   int rc;
-  const size_t dinv_bytes = (size_t)nbk * 32 * 32 * sizeof(double);
+  // chain-bound steps: (K-1, K) pass counts below this trailing size (see below)
+  const int k_par = b <= 128 ? 48 : (b <= 256 ? 26 : (b <= 384 ? 22 : 18));
+  // Dinv blocks of one diagonal tile per step of a multi-step launch
+  const int max_multi = (k_par + 2 < T ? k_par + 2 : T);
+  const size_t dinv_bytes = (size_t)max_multi * nbk * 32 * 32 * sizeof(double);
   if ((rc = ensure(ctx, (void**)&ctx->d_dinv, &ctx->dinv_cap, dinv_bytes))) return rc;
   // per-step gate block: [0, T-J-1) column-(J+1) tile counters, [T] inverse
   // published, [T+1] look-ahead ticket, [T+2] POTRF progress (substitution
@@ -265,6 +270,14 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   // chain-bound steps at tiles >= 256: fused TRSM by substitution (BGP_TRSM_SUBST=0: inverse + GEMM)
   static const bool trsm_subst = [] {
     const char* e = getenv("BGP_TRSM_SUBST");
+    return !(e && atoi(e) == 0);
+  }();
+  // the chain-bound steps of the last level in ONE launch ordered by
+  // counters (BGP_MULTI_STEP=0: one launch per step).  Not in a context
+  // with a grid cap (a pipelined lane sharing the GPU): its waiting CTAs
+  // would hold SMs that per-step launches hand back to the other lanes.
+  static const bool multi_step = [] {
+    const char* e = getenv("BGP_MULTI_STEP");
     return !(e && atoi(e) == 0);
   }();
   if (trsm_par) {
@@ -317,6 +330,45 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     double* dkk = tiles + tri_index(K, K, T) * tsz;
     int* gate = ctx->d_gate + (int64_t)J * stride;
     StepMarks sm{-1, -1, -1, -1};
+    if (multi_step && ctx->grid_cap <= 0 && trsm_subst && la_mode == 1 && J_stop == T && T - J - 1 <= k_par && T - 1 - J >= 2 &&
+        T - 1 - J <= max_multi) {
+      // steps J .. T-2 (every remaining one) in one launch: per-tile update
+      // counters, per-tile solve counters, per-step POTRF progress, queue
+      const int ns = T - 1 - J;
+      const int64_t nt = tri_count(T - J - 1);
+      const size_t words = (size_t)(2 * nt + ns + 8);
+      if ((rc = ensure(ctx, (void**)&ctx->d_multi, &ctx->multi_cap, words * sizeof(int)))) return rc;
+      cudaError_t e = cudaMemsetAsync(ctx->d_multi, 0, words * sizeof(int), s);
+      if (e != cudaSuccess) return set_err(ctx, "multi-step counters", e);
+      int* base = ctx->d_multi;
+      GemmProblem p{};
+      p.mode = GEMM_CHOL_TRAIL;
+      p.b = b;
+      p.T = T;
+      p.J = J;
+      p.nsteps = ns;
+      p.alpha = -1.0;
+      p.beta = 1.0;
+      p.check_info = true;
+      p.tile_cnt = base;
+      p.solved = base + nt;
+      p.potrf_progress = base + 2 * nt;
+      p.queue = base + ((2 * nt + ns + 1) & ~(int64_t)1);  // 64-bit aligned
+      p.role_ticket = p.queue + 2;
+      p.n_live = n;
+      p.trsm_next = 1;
+      p.trsm_subst = 1;
+      p.tile_need = tile_need;
+      p.diag_need = diag_need;
+      p.potrf_tile = dkk;
+      p.potrf_row0 = row_base + (int64_t)K * b;
+      p.dinv = ctx->d_dinv;
+      if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
+      sm.gemm_end = sm.t_end = mk.mark(s);
+      for (int Js = J; Js < J_last && Js < 4096; ++Js)
+        if (sm_out) sm_out[Js] = sm;  // (one mark for the whole launch)
+      break;
+    }
     GemmProblem p{};
     p.mode = GEMM_CHOL_TRAIL;
     p.b = b;
@@ -348,7 +400,6 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
         // work shorter than POTRF + inverse + solve): there the groups
         // waiting on passes to their right are idle anyway, while in large
         // steps the waits would cost update throughput
-        const int k_par = b <= 128 ? 48 : (b <= 256 ? 26 : (b <= 384 ? 22 : 18));
         if (trsm_subst && T - J - 1 <= k_par) {
           // the panel solve by substitution follows the POTRF block by block
           // (no tile inverse; 128 tiles are then factored in place too)

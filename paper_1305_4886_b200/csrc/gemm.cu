@@ -171,8 +171,47 @@ __host__ __device__ __forceinline__ bool gemm_task_kind(const GemmProblem& p, in
   return false;
 }
 
-__host__ __device__ __forceinline__ int64_t gemm_num_tasks(const GemmProblem& p) {
+__host__ __device__ __forceinline__ int64_t gemm_step_tasks(const GemmProblem& p) {
   return p.mode == GEMM_TRSM_PANEL ? gemm_trsm_tasks(p) : gemm_num_items(p) + gemm_trsm_tasks(p);
+}
+
+// Multi-step launch (nsteps > 1): the view of step s as a one-step problem
+// (its update by panel s, then the solve of panel s+1 unless s+1 is the last
+// tile row); the TRSM tasks follow the step's column-(s+1) blocks directly
+// (no tail filler: these steps are chain-bound).
+__host__ __device__ __forceinline__ void multi_step_view(const GemmProblem& p, int s, GemmProblem& ps) {
+  ps = p;
+  ps.J = s;
+  ps.nsteps = 1;
+  ps.trsm_next = (s + 2 < p.T);
+  ps.trsm_tail = 0;
+}
+// task -> step s and the task's index inside step s's list
+__host__ __device__ __forceinline__ int multi_locate(const GemmProblem& p, int64_t task, GemmProblem& ps,
+                                                     int64_t& local) {
+  int s = p.J;
+  for (;;) {
+    multi_step_view(p, s, ps);
+    const int64_t n = gemm_step_tasks(ps);
+    if (task < n || s + 1 >= p.J + p.nsteps) break;
+    task -= n;
+    ++s;
+  }
+  local = task;
+  return s;
+}
+
+__host__ __device__ __forceinline__ int64_t gemm_num_tasks(const GemmProblem& p) {
+  if (p.mode == GEMM_CHOL_TRAIL && p.nsteps > 1) {
+    int64_t n = 0;
+    GemmProblem ps;
+    for (int s = p.J; s < p.J + p.nsteps; ++s) {
+      multi_step_view(p, s, ps);
+      n += gemm_step_tasks(ps);
+    }
+    return n;
+  }
+  return gemm_step_tasks(p);
 }
 
 // diagonal-tile block (bi, bj): skip blocks strictly above the diagonal,
@@ -430,6 +469,9 @@ __device__ __forceinline__ uint64_t* stagger_bar(uint8_t* smem) {
 // tmT: the C tiles with the operand box -- the A operand of an in-place TRSM
 // block (the tile it solves), which differs from tmA when A / B are a panel
 // buffer (the distributed sweep step)
+// MULTI: the multi-step launch (nsteps > 1) -- a separate instantiation so
+// the one-step path's code is unchanged by the per-task step lookup
+template <bool MULTI>
 __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtensorMap* tmA,
                                               const CUtensorMap* tmB, const CUtensorMap* tmL,
                                               const CUtensorMap* tmT, const GemmProblem& p,
@@ -443,32 +485,61 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
   const int64_t ntasks = gemm_num_tasks(p);
   int stage = 0;
   uint32_t phase = 0;
+  constexpr bool multi = MULTI;
+  GemmProblem ps;  // multi: the claimed task's step as a one-step problem
   for (;;) {
-    const int64_t task = atomicAdd(reinterpret_cast<unsigned long long*>(p.queue), 1ull);
+    int64_t task = atomicAdd(reinterpret_cast<unsigned long long*>(p.queue), 1ull);
     if (task >= ntasks) break;
+    int step = p.J;
+    if constexpr (MULTI) step = multi_locate(p, task, ps, task);
+    const GemmProblem& q = MULTI ? ps : p;
     int64_t idx;
-    if (gemm_fused_trsm(p) && gemm_task_kind(p, task, idx)) {
+    if (gemm_fused_trsm(q) && gemm_task_kind(q, task, idx)) {
       // fused TRSM of panel J+1: the tile's update blocks have retired and
       // (Cholesky) the look-ahead CTA published Linv(J+1); the kriging solve's
       // inverses are computed up front (no flag)
-      const int per_tile = (p.b / BM) * (gemm_par_passes(p) ? p.b / BN : 1);
+      const int per_tile = (p.b / BM) * (gemm_par_passes(q) ? p.b / BN : 1);
       const int tile = (int)(idx / per_tile);
       if (stagger) {  // group 0: release group 1 before blocking (see consumer_loop)
         mbar_arrive(stagger);
         stagger = nullptr;
       }
-      const int g0 = p.mode == GEMM_RECT_TRAIL ? 0 : 1;  // Cholesky gate 0 is the diagonal tile
-      if (!wait_count(p.col_gate + g0 + tile, p.tile_need, info) ||
-          (p.linv_flag && !p.trsm_subst && !wait_count(p.linv_flag, p.linv_need, info)))
-        break;
+      if (multi) {  // tile (step+2+tile, step+1): the updates of steps J .. step retired
+        const int64_t t = tri_index(step + 2 + tile, step + 1, p.T) - p.cnt_base;
+        if (!wait_count(p.tile_cnt + t, (step + 1 - p.J) * p.tile_need, info)) break;
+      } else {
+        const int g0 = p.mode == GEMM_RECT_TRAIL ? 0 : 1;  // Cholesky gate 0 is the diagonal tile
+        if (!wait_count(p.col_gate + g0 + tile, p.tile_need, info) ||
+            (p.linv_flag && !p.trsm_subst && !wait_count(p.linv_flag, p.linv_need, info)))
+          break;
+      }
       fence_proxy_async_global();
+    } else if (multi && step > p.J) {
+      // update by panel `step`, solved inside this launch: wait for its two
+      // panel tiles (generic stores of the substitution -> TMA reads)
+      const Item i0 = gemm_decode(q, task, 0);
+      if (i0.valid) {
+        if (stagger) {
+          mbar_arrive(stagger);
+          stagger = nullptr;
+        }
+        if (!wait_count(p.solved + (i0.aTile0 - p.cnt_base), p.solved_need, info) ||
+            !wait_count(p.solved + (i0.bTile0 - p.cnt_base), p.solved_need, info))
+          break;
+        fence_proxy_async_global();
+      }
     }
-    const int npass = gemm_task_passes(p, task);
+    const int npass = gemm_task_passes(q, task);
     for (int pass = 0; pass < npass; ++pass) {
-      const Item it = gemm_decode(p, task, pass);
+      Item it = gemm_decode(q, task, pass);
+      // multi: every update block counts toward its C tile (solves and
+      // factorizations of later steps wait on them)
+      if (multi && !it.subst && !it.bLinv) it.gate = (int)(it.cTile - p.cnt_base);
       if (!it.valid) {
         // a padding block counts toward its tile's gate as if it had retired
         if (it.pad && it.gate >= 0) atomicAdd(p.col_gate + it.gate, GROUP_WARPS);
+        // (multi) a padding slab counts as solved
+        if (it.pad && multi && it.subst) atomicAdd(p.solved + (it.cTile - p.cnt_base), GROUP_WARPS);
         continue;
       }
       if (it.subst) {
@@ -486,6 +557,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
         sl.slab = -1;
         sl.pass = 0;
         sl.pad[0] = 1;
+        sl.pad[1] = step - p.J;  // multi: the step (its factor, Dinv and progress)
         mbar_arrive(&gs.full[stage]);
         if (++stage == STAGES) {
           stage = 0;
@@ -516,7 +588,7 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
         const int kt = kc / kc_per_tile;
         const int kin = (kc % kc_per_tile) * BK;
         const int at = (int)(it.aTile0 + kt * it.aStride);
-        const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, p.T)
+        const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, q.T)
                                        : (int)(it.bTile0 + kt * it.bStride);
         BGP_CHECK(at >= 0 && at < (ta == tmT ? p.nC : p.nA));
         BGP_CHECK(bt >= 0 && bt < (it.bLinv ? 1 : p.nB));
@@ -738,6 +810,7 @@ __device__ __noinline__ void trsm_subst_rows(int b, const double* __restrict__ L
   }
 }
 
+template <bool MULTI>
 __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gwarp, int lane,
                                               const CUtensorMap* tmC, const GemmProblem& p,
                                               uint64_t* stagger, const PushMaps* pm,
@@ -797,9 +870,17 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         if (lane == 0) mbar_arrive(stagger);
         stagger_arrive = false;
       }
-      trsm_subst_rows(p.b, p.potrf_tile, p.dinv, p.potrf_progress, p.cbase + (int64_t)it.cTile * p.b * p.b,
-                      it.mrow0 + 32 * gwarp, lane, info, pm, p.npush, (int64_t)it.cTile - p.panel0);
+      // the step's factor, Dinv blocks and progress counter (multi: step J + pad[1])
+      const int so = MULTI ? it.pad[1] : 0;
+      const double* ptile = MULTI ? p.cbase + tri_index(p.J + so + 1, p.J + so + 1, p.T) * p.b * p.b : p.potrf_tile;
+      trsm_subst_rows(p.b, ptile, p.dinv + (int64_t)so * p.b * 32, p.potrf_progress + so,
+                      p.cbase + (int64_t)it.cTile * p.b * p.b, it.mrow0 + 32 * gwarp, lane, info, pm, p.npush,
+                      (int64_t)it.cTile - p.panel0);
       __syncwarp();
+      if (MULTI && lane == 0) {  // rows solved: later steps' update blocks read them by TMA
+        __threadfence();
+        atomicAdd(p.solved + (it.cTile - p.cnt_base), 1);
+      }
       if (lane == 0) mbar_arrive(&gs.empty[stage]);
       if (++stage == STAGES) {
         stage = 0;
@@ -938,7 +1019,9 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
         tma_store_wait_all0();
         fence_proxy_async_global();
         __threadfence();
-        BGP_CHECK(it.gate < (p.mode == GEMM_LIST ? p.trsm_count + 1 : (p.mode == GEMM_RECT_TRAIL ? p.Tm : p.T)));
+        BGP_CHECK(it.gate < (MULTI ? tri_count(p.T - p.J - 1)
+                                          : (p.mode == GEMM_LIST ? p.trsm_count + 1
+                                                                 : (p.mode == GEMM_RECT_TRAIL ? p.Tm : p.T))));
         atomicAdd(p.col_gate + it.gate, 1);
       }
       __syncwarp();
@@ -950,6 +1033,8 @@ __device__ __forceinline__ void consumer_loop(const GroupSmem& gs, int g, int gw
   if (p.npush > 0) __threadfence_system();  // pushed panel visible to the peers
 }
 
+// MULTI: the multi-step tail launch (nsteps > 1), its own instantiation
+template <bool MULTI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmC,
@@ -986,7 +1071,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     if (lookahead_cta) named_bar_sync(1, THREADS);  // wait for the panel work below
     if (warp < GROUPS && lane == 0)
-      producer_loop(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmT, p, info, warp == 0 ? stagger_bar(smem) : nullptr);
+      producer_loop<MULTI>(group_smem(smem, warp), &tmA, &tmB, &tmL, &tmT, p, info,
+                           warp == 0 ? stagger_bar(smem) : nullptr);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
     if (lookahead_cta) {
@@ -994,7 +1080,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the ring memory once the update blocks of the diagonal tile retired;
       // other CTAs' TRSM tasks wait for the published inverse
       const int ctid = threadIdx.x - 128;
-      if (ctid < 256) {
+      if (MULTI && ctid < 256) {
+        // multi-step launch: factor (K, K) for K = J+1 .. J+nsteps one after
+        // another, each once the updates of steps J .. K-1 into it retired;
+        // the substitution solves follow each through its progress counter
+        double* psm = reinterpret_cast<double*>(smem);
+        for (int K = p.J + 1; K <= p.J + p.nsteps && K < p.T; ++K) {
+          const int64_t dt = tri_index(K, K, p.T);
+          if (ctid == 0) s_go = wait_count(p.tile_cnt + (dt - p.cnt_base), (K - p.J) * p.diag_need, info) ? 1 : 0;
+          named_bar_sync(2, 256);
+          if (!s_go) break;
+          const bool ok = tile_potrf_inv_device(p.cbase + dt * p.b * p.b, p.b, p.potrf_row0 + (int64_t)(K - p.J - 1) * p.b,
+                                                p.dinv + (int64_t)(K - p.J - 1) * p.b * 32, info, nullptr, psm, ctid, 2,
+                                                p.potrf_progress + (K - p.J - 1));
+          named_bar_sync(2, 256);  // (shared memory and s_go reused by the next factorization)
+          if (!ok) break;
+        }
+      } else if (ctid < 256) {
         double* psm = reinterpret_cast<double*>(smem);
         if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
         named_bar_sync(2, 256);
@@ -1010,7 +1112,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       named_bar_sync(1, THREADS);  // release this CTA's producers
     }
     const int g = wg - 1;
-    consumer_loop(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm, info);
+    consumer_loop<MULTI>(group_smem(smem, g), g, warp & 3, lane, &tmC, p, stagger_bar(smem), &pm, info);
   }
 }
 
@@ -1032,9 +1134,11 @@ int groups() { return GROUPS; }
 void prepare() {
   static int occupancy = -1;
   if (occupancy < 0) {
-    cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(gemm_dmma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, gemm_dmma_kernel, THREADS, SMEM_BYTES);
+    for (auto k : {gemm_dmma_kernel<false>, gemm_dmma_kernel<true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, gemm_dmma_kernel<false>, THREADS, SMEM_BYTES);
     if (occupancy < 1) fprintf(stderr, "libbgp: gemm_dmma_kernel cannot be resident\n");
   }
 }
@@ -1044,6 +1148,14 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   if (p_in.b % BM != 0) return set_err(ctx, "gemm: tile must be a multiple of 128", cudaErrorInvalidValue);
   GemmProblem p = p_in;
   p.cbase = Cbase;
+  if (p.nsteps > 1) {
+    if (p.mode != GEMM_CHOL_TRAIL || !p.trsm_subst || !p.tile_cnt || !p.solved || !p.potrf_progress ||
+        !p.potrf_tile)
+      return set_err(ctx, "gemm: bad multi-step launch", cudaErrorInvalidValue);
+    p.col_gate = p.tile_cnt;
+    p.solved_need = (p.b / BM) * GROUP_WARPS;
+    p.cnt_base = tri_index(p.J + 1, p.J + 1, p.T);
+  }
   p.nA = nA;
   p.nB = nB;
   p.nC = nC;
@@ -1083,8 +1195,12 @@ int launch(Ctx* ctx, const GemmProblem& p_in, double* Cbase, const double* Abase
   // the look-ahead CTA's device POTRF / inverse must fit the ring memory
   if (p.potrf_tile && tile_potrf_inv_smem_bytes(p.b, true) > (size_t)(GROUPS * GROUP_BYTES))
     return set_err(ctx, "gemm: look-ahead POTRF does not fit", cudaErrorInvalidValue);
-  gemm_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, mT, p,
-                                                                  p.check_info ? ctx->d_info : nullptr, pm);
+  if (p.nsteps > 1)
+    gemm_dmma_kernel<true><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, mT, p,
+                                                                        p.check_info ? ctx->d_info : nullptr, pm);
+  else
+    gemm_dmma_kernel<false><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mB, mL, mC, mT, p,
+                                                                         p.check_info ? ctx->d_info : nullptr, pm);
   ctx->launches++;
   return check_launch(ctx, "gemm_dmma");
 }
