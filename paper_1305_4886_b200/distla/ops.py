@@ -274,8 +274,10 @@ def cholesky(ctx, name, out_name):
             ctx.comm.timeline = tl
             ctx.synchronize()
             t0 = time.perf_counter()
+            ops = LibTileOps(ctx, obj.n, tl)
             try:
-                info.value = dist_cholesky(obj.dist, obj.data, LibTileOps(ctx, obj.n, tl), ctx.comm)
+                info.value = dist_cholesky(obj.dist, obj.data, ops, ctx.comm)
+                peak_tiles = getattr(ops, "peak_tiles", obj.dist.storage_count)
             finally:
                 ctx.comm.timeline = None
             ctx.synchronize()
@@ -290,10 +292,20 @@ def cholesky(ctx, name, out_name):
         ctx.store.pop(out_name, None)
         raise NotPositiveDefinite((info.value - 1) // obj.row_layout.block_size + 1)
     ctx.log_event("factor")
-    if obj.dist is not None:  # owned tiles, and the shadow diagonal tiles held besides
-        return {"peak_blocks": obj.dist.storage_count, "owned_blocks": obj.dist.count, "tile": obj.tile}
+    # peak_blocks in the reference's unit (row-layout blocks, bg/distla/
+    # kernels.py: blocks resident at the peak): this rank's resident device
+    # elements / block_size^2.  Distributed: owned tiles, shadow diagonal
+    # tiles, the two panel-exchange buffers and the gathered tail; the
+    # panel buffers (2 x T tiles) dominate at small n
+    bs2 = float(obj.row_layout.block_size) ** 2
+    t2 = float(obj.tile) ** 2
+    if obj.dist is not None:
+        return {"peak_blocks": peak_tiles * t2 / bs2, "owned_blocks": obj.dist.count * t2 / bs2,
+                "tile": obj.tile, "peak_tiles": int(peak_tiles), "storage_tiles": obj.dist.storage_count,
+                "owned_tiles": obj.dist.count}
     nt = obj.data.shape[0]
-    return {"peak_blocks": nt, "owned_blocks": nt, "tile": obj.tile}
+    return {"peak_blocks": nt * t2 / bs2, "owned_blocks": nt * t2 / bs2, "tile": obj.tile, "peak_tiles": nt,
+            "storage_tiles": nt, "owned_tiles": nt}
 
 
 @registry.register("distla.loglik_many")

@@ -305,6 +305,12 @@ def dist_cholesky(dist, local, ops, comm):
         if xchg is None and J + 1 < min(T - 1, J0):
             broadcast_panel(J + 1)
     info = comm.min_nonzero(ops.end())
+    # resident tiles at the peak (reported by distla.cholesky): my storage,
+    # the two panel buffers, and the gathered tail triangle (+ my share)
+    pbuf = 2 * xchg.tiles if xchg is not None else sum(p.shape[0] for p in panels if p is not None)
+    T2 = T - J0
+    ops.peak_tiles = dist.storage_count + pbuf + (T2 * (T2 + 1) // 2 + T2 * T2 // max(dist.grid.G, 1)
+                                                  if J0 < T else 0)
     if J0 < T and not info:
         info = comm.min_nonzero(factor_tail(dist, local, ops, comm, J0))
     return info

@@ -65,7 +65,7 @@ def _worker(rank, world, port, q, xfer="push"):
         out["x"] = distla.collect(cl, x)
         out["logdet"] = distla.log_det_from_chol(cl, L)
         assert len(stats) == world  # per-rank stats, gathered
-        out["owned"] = stats[rank]["owned_blocks"]
+        out["owned"] = stats[rank]["owned_tiles"]
         # NotPositiveDefinite is agreed by every rank and leaves no factor
         Cn = distla.distribute(cl, "Cn", -np.eye(300), "triangular", distla.make_layout(300, cl.grid, h=1))
         try:
@@ -167,7 +167,7 @@ def test_master_spawn_reference_call_sequence():
         L, stats = distla.distributed_cholesky(cl, C, "L")
         assert len(stats) == 2
         T = -(-n // 128)
-        assert sum(s["owned_blocks"] for s in stats) == T * (T + 1) // 2
+        assert sum(s["owned_tiles"] for s in stats) == T * (T + 1) // 2
         assert relerr(distla.collect(cl, L), np.linalg.cholesky(A)) <= 1e-12
         parts = cl.run("distla.logdet", l_name="L")
         assert len(parts) == 2
