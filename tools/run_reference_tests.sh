@@ -21,8 +21,8 @@ OUT=${2:-gpurun_out/reftests.txt}
 DESEL="not test_memory_instrument_bound and not test_critical_path_event_order"
 DESEL="$DESEL and not criterion_1_ and not criterion_6_ and not criterion_7_"
 DESEL="$DESEL and not criterion_8_ and not criterion_10_"
-# (criteria 2, 3 and 4 share one test; criterion 4 is the reference's
-# per-worker block-count instrument of its triangular layout, not applicable)
+# (criteria 2, 3 and 4 share one test; criterion 4 reads the backend's
+# peak_blocks, reported in the reference's unit)
 PYTHONPATH=tools/reftests:. python -m pytest baseline/_ref/tests -v -s -p no:cacheprovider \
   -k "$DESEL" -rf > "$OUT" 2>&1 || true
 tail -5 "$OUT"
