@@ -747,7 +747,8 @@ class LibTileOps:
         on first use), or None for NCCL broadcasts (BGP_PANEL_XFER=nccl, one
         rank, or a failed self-check)."""
         import os
-        if comm.world == 1 or os.environ.get("BGP_PANEL_XFER", "push") != "push":
+        # (one push destination per rank, at most BGP_MAX_PUSH = 8: one node)
+        if comm.world == 1 or comm.world > 8 or os.environ.get("BGP_PANEL_XFER", "push") != "push":
             return None
         cache = self.cl.__dict__.setdefault("_panel_xchg", {})
         x = cache.get("x")
