@@ -115,8 +115,10 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen,
  * diagonal tile (building its inverse during the factorization, or
  * publishing its progress per 32 columns for a substitution solve) once that
  * tile's update blocks have retired, and the next panel's solve runs as
- * gated tasks of the same launch.  Every wait is inside the launch, so the
- * schedule also holds when kernels are serialised (Nsight Compute).
+ * gated tasks of the same launch; the chain-bound steps of
+ * the last level run as ONE launch ordered by per-tile counters.  Every wait
+ * is inside a launch, so the schedule also holds when kernels are serialised
+ * (Nsight Compute).
  * BGP_LOOKAHEAD=0 in the environment runs POTRF, inverse, solve and update
  * as separate launches one after another on `stream` (diagnostics). */
 int bgp_potrf(bgp_ctx_t ctx, double* tiles, int64_t n, int tile,

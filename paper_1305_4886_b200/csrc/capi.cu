@@ -214,7 +214,9 @@ int bgp_construct(bgp_ctx_t ctx, int kind, const bgp_generator* gen, const doubl
 // the inverse.  So the latency-bound POTRF and the panel TRSM both run under
 // the trailing update.  Waits are one-way (update blocks -> POTRF -> TRSM
 // tasks, never back), bounded, and reported as errors if they time out.  The
-// only host synchronization is the final status read.
+// chain-bound steps of the last level (the tail) run as ONE launch whose task
+// lists follow one another, ordered by per-tile counters (GemmProblem
+// nsteps).  The only host synchronization is the final status read.
 // Event marks of one bgp_potrf call (profiling only).
 struct Marks {
   Ctx* ctx;
