@@ -20,7 +20,10 @@
 // consumers through the ring (dynamic scheduling: no static imbalance).
 // A trailing-update launch can append the TRSM of the next panel as tasks:
 // their producer waits, per tile, until the update blocks of that tile have
-// retired and the side stream published the tile inverse.
+// retired, and the launch's look-ahead CTA factors the next diagonal tile
+// (publishing its inverse, or its progress for a substitution solve).  The
+// chain-bound tail runs several steps per launch (nsteps > 1), ordered by
+// per-tile counters.
 //
 // Bank conflicts: a 16-double-wide TMA box with 128B swizzle stores element
 // (mn, k) at chunk ((mn&15)>>1) ^ (k&7).  Each MMA k4 step takes
