@@ -130,3 +130,56 @@ def test_large_steps_keep_serial_passes(cluster_factory):
     L, _ = distla.distributed_cholesky(cl, C, "L")
     got = distla.collect(cl, L)
     assert relerr(got, np.linalg.cholesky(A)) <= 1e-12
+
+
+@pytest.mark.parametrize("tile,bad_tile", [(128, 1), (128, 5), (128, 8), (256, 2), (256, 6)])
+def test_multistep_tail_failure_positions(cluster_factory, tile, bad_tile):
+    """Failures inside the multi-step tail launch (every step chain-bound at
+    these sizes): the first, a middle and the last diagonal tile.  The
+    launch stops at the failing factorization (no hang), reports the block,
+    leaves no factor, and the next factorization on the cluster is right."""
+    from paper_1305_4886_b200 import distla
+    from paper_1305_4886_b200.errors import NotPositiveDefinite
+    n = tile * 9 - 11
+    A = spd_matrix(n, seed=bad_tile)
+    bad = min(bad_tile * tile + 17, n - 1)
+    A[bad, bad] = -1.0
+    cl = cluster_factory(tile=tile)
+    lay = distla.make_layout(n, cl.grid, h=5)
+    C = distla.distribute(cl, "C", A, "triangular", lay)
+    with pytest.raises(NotPositiveDefinite) as info:
+        distla.distributed_cholesky(cl, C, "L")
+    assert info.value.block_index == bad // lay.block_size + 1
+    assert "L" not in set(cl.remote_ls())
+    A2 = _cov(n, seed=bad_tile)
+    C2 = distla.distribute(cl, "C2", A2, "triangular", lay)
+    L2, _ = distla.distributed_cholesky(cl, C2, "L2")
+    assert relerr(distla.collect(cl, L2), np.linalg.cholesky(A2)) <= 1e-12
+
+
+def test_one_launch_per_step_fallback_matches(tmp_path):
+    """BGP_MULTI_STEP=0 (one launch per step in the chain-bound tail, read
+    once per process) gives the same factor as the default multi-step
+    launch, both against LAPACK."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from conftest import spd_matrix\n"
+        "from paper_1305_4886_b200 import distla, spawn\n"
+        "cl = spawn(1, tile=128); n = 128 * 12 - 5; A = spd_matrix(n, seed=2)\n"
+        "C = distla.distribute(cl, 'C', A, 'triangular', distla.make_layout(n, cl.grid, h=3))\n"
+        "L, _ = distla.distributed_cholesky(cl, C, 'L'); np.save(sys.argv[1], distla.collect(cl, L))\n"
+        "cl.shutdown()\n") % (root, os.path.join(root, "tests"))
+    out = {}
+    for m in ("0", "1"):
+        f = str(tmp_path / f"L{m}.npy")
+        env = dict(os.environ, BGP_MULTI_STEP=m)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=env, timeout=600)
+        out[m] = np.load(f)
+    n = out["0"].shape[0]
+    want = np.linalg.cholesky(spd_matrix(n, seed=2))
+    assert relerr(out["0"], want) <= 1e-12 and relerr(out["1"], want) <= 1e-12
+    assert relerr(out["0"], out["1"]) <= 1e-13
