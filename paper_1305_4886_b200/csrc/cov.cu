@@ -9,10 +9,11 @@
 // their points in registers, reads each column point once from shared
 // memory (16-byte loads) and writes both entries of a column with one
 // 16-byte store -- a warp stores 512 contiguous bytes per column.  Per entry
-// it spends ~23 FP64 instructions: difference, squared distance (one FMA),
-// sqrt, one multiply by sqrt(2 nu)/rho, and exp by a 64-entry table of
-// sigma^2 2^(j/64) (so the variance costs nothing) with a degree-5 polynomial
-// and magic-number rounding (no FP64<->int conversions, no branch).  The
+// it spends ~17 FP64 instructions: difference and squared distance of
+// points pre-scaled by sqrt(2 nu)/rho (so s = sqrt(q) directly), sqrt, and
+// exp by a 256-entry table of sigma^2 2^(j/256) (so the variance costs
+// nothing) with a one-step reduction, a degree-4 polynomial and
+// magic-number rounding (no FP64<->int conversions, no branch).  The
 // kernel is bound by the HBM write stream (8 B per entry) and the FP64 issue
 // rate together.
 //
@@ -29,9 +30,12 @@ namespace bgp {
 
 constexpr int kMaxDim = 4;
 #ifndef COV_UNROLL
-#define COV_UNROLL 8
+#define COV_UNROLL 4
 #endif
 constexpr int kCovUnroll = COV_UNROLL;  // columns per unrolled iteration of the fast path (2 entries each)
+#ifndef COV_MIN_BLOCKS
+#define COV_MIN_BLOCKS 1
+#endif
 
 __device__ __forceinline__ double matern_corr(double d, double rho, double sqrt2nu, int nucode) {
   // bg/gp/kernels.py:16-29: s = sqrt(2 nu) * d / rho
@@ -94,62 +98,69 @@ constexpr int kCovThreads = 256;
 
 // Fast path for the common generators in 2-D (KIND 1..3: Matern nu = 1/2,
 // 3/2, 5/2; KIND 4: squared exponential); KIND 0 is the generic path.
-__device__ double kExp2Tab[64];  // 2^(j/64), host-computed (init_exp_table)
+constexpr int kExpTab = 256;
+__device__ double kExp2Tab[kExpTab];  // 2^(j/256), host-computed (init_exp_table)
 
-// sigma^2 exp(x) for x <= 0: x 64/ln2 = k + f by magic-number rounding
-// (k in the low word of t), exp(x) = 2^(k>>6) 2^((k&63)/64) exp(r),
-// |r| <= ln2/128, exp(r) by a degree-5 polynomial (truncation < 4e-17); the
-// table holds sigma^2 2^(j/64).  Below 2^-1020 the result is 0 (the
-// reference's exp underflows there as well, to within 1e-307).
+// sigma^2 exp(x) for x <= 0: x 256/ln2 = k + f by magic-number rounding
+// (k in the low word of t), exp(x) = 2^(k>>8) 2^((k&255)/256) exp(r),
+// r = x - k ln2/256 in one FMA (|r| <= ln2/512; the rounding of ln2/256
+// costs |k| 2^-61 ~ |x| 1e-16 relative, i.e. under 4e-17 of the result),
+// exp(r) by a degree-4 polynomial (truncation < 4e-17); the table holds
+// sigma^2 2^(j/256).  Below 2^-1020 the result is 0 (the reference's exp
+// underflows there as well, to within 1e-307).
 // constant-bank operands of the fast path's FP64 instructions (an FP64
 // immediate must have a zero low word; these do not)
-__constant__ double kExpC[6] = {92.33248261689366, -0.010830424696249145, -3.623510646634843e-19,
-                                1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+__constant__ double kExpC[4] = {369.3299304675746, -0.0027076061740622863, 1.0 / 24.0, 1.0 / 6.0};
 template <bool SAFE>
 __device__ __forceinline__ double exp_scaled(double x, const double* __restrict__ tab) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
-  const double t = fma(x, kExpC[0], magic);  // x 64 / ln2
+  const double t = fma(x, kExpC[0], magic);  // x 256 / ln2
   const double kd = t - magic;
   const int k = __double2loint(t);
-  double r = fma(kd, kExpC[1], x);  // Cody-Waite: ln2/64 = hi + lo
-  r = fma(kd, kExpC[2], r);
-  double p = fma(r, kExpC[3], kExpC[4]);
-  p = fma(r, p, kExpC[5]);
+  const double r = fma(kd, kExpC[1], x);
+  double p = fma(r, kExpC[2], kExpC[3]);
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
-  const int n = k >> 6;  // k <= 0: arithmetic shift floors
-  const double v = tab[k & 63] * p;
+  const int n = k >> 8;  // k <= 0: arithmetic shift floors
+  const double v = tab[k & (kExpTab - 1)] * p;
   const double w = __hiloint2double(__double2hiint(v) + (n << 20), __double2loint(v));
   return (SAFE || n >= -1020) ? w : 0.0;  // SAFE: the host's distance bound rules underflow out
 }
 
 // sqrt(q), q >= 0, to ~1 ulp without the library's special-case branch:
-// hardware rsqrt seed, one cubic correction (y = q^-1/2 to ~2^-70), d = q y.
-// q below 2^-1022 (coincident points) is raised to 2^-1022 by one integer
-// max on its high word: d = 2^-511, which every kernel maps to corr = 1, as
-// for d = 0.
+// hardware rsqrt seed y, d0 = q y, and one cubic correction of d0 itself,
+// d0 (1 + e/2 + 3e^2/8) with e = 1 - d0 y (five FP64 instructions).  q below
+// 2^-1022 (coincident points) is raised to 2^-1022 by one integer max on its
+// high word: d = 2^-511, which every kernel maps to corr = 1, as for d = 0.
 __device__ __forceinline__ double sqrt_fast(double q) {
   q = __hiloint2double(max(__double2hiint(q), 0x00100000), __double2loint(q));
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
-  const double e = fma(-q, y * y, 1.0);
-  y = fma(y * e, fma(e, 0.375, 0.5), y);
-  return q * y;
+  const double d0 = q * y;
+  const double e = fma(-d0, y, 1.0);
+  return fma(d0 * e, fma(e, 0.375, 0.5), d0);
 }
 
-// sigma^2 * corr(d) for the fast path from the squared distance q; sc =
-// sqrt(2 nu) / rho (Matern) or 1 / rho (squared exponential).  KIND & 7:
-// 1..3 Matern nu = 1/2, 3/2, 5/2, 4 squared exponential; KIND & 8: no
-// underflow test (GenDev.safe_exp)
+// the fast path's coordinate scale (1 for the generic path, KIND 0)
 template <int KIND>
-__device__ __forceinline__ double cov_fast(double q, double sc, const double* __restrict__ tab) {
+__device__ __forceinline__ double cov_scale(const GenDev& g) {
+  if constexpr ((KIND & 7) == 0) return 1.0;
+  else return (KIND & 7) == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
+}
+
+// sigma^2 * corr(d) for the fast path from q = (sc d)^2, the squared
+// distance of points pre-scaled by sc = sqrt(2 nu) / rho (Matern) or 1 / rho
+// (squared exponential).  KIND & 7: 1..3 Matern nu = 1/2, 3/2, 5/2, 4 squared
+// exponential; KIND & 8: no underflow test (GenDev.safe_exp)
+template <int KIND>
+__device__ __forceinline__ double cov_fast(double q, const double* __restrict__ tab) {
   constexpr int K = KIND & 7;
   constexpr bool SAFE = (KIND & 8) != 0;
-  if (K == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 (d/rho)^2) = exp(-0.5 q / rho^2)
-    return exp_scaled<SAFE>(-0.5 * (q * (sc * sc)), tab);
+  if (K == 4) {  // bg/gp/kernels.py:32-34: exp(-0.5 (d/rho)^2)
+    return exp_scaled<SAFE>(-0.5 * q, tab);
   }
-  const double sv = sqrt_fast(q) * sc;  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) d / rho
+  const double sv = sqrt_fast(q);  // bg/gp/kernels.py:16-29: s = sqrt(2 nu) d / rho
   const double e = exp_scaled<SAFE>(-sv, tab);
   if (K == 1) return e;
   if (K == 2) return fma(sv, e, e);
@@ -171,9 +182,13 @@ __device__ __forceinline__ void cov_tile_fast(const GenDev& g, const double* __r
   if (part >= nsplit) return;
   const int r = 2 * pr, cw = b / nsplit, c0 = part * cw;
   const int64_t ia = i0 + r, ib = ia + 1;
-  const double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ia, n - 1) : ia));
-  const double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ib, n - 1) : ib));
-  const double sc = (KIND & 7) == 4 ? 1.0 / g.p[1] : g.sqrt2nu / g.p[1];
+  // row points pre-scaled by sc like the column points in shared memory
+  // (the scaled difference carries the same ~|x| sc 1e-16 absolute rounding
+  // as the reference's unscaled one times sc)
+  const double sc = cov_scale<KIND>(g);
+  double2 x0 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ia, n - 1) : ia));
+  double2 x1 = *reinterpret_cast<const double2*>(X + 2 * (PAD ? min(ib, n - 1) : ib));
+  x0.x *= sc, x0.y *= sc, x1.x *= sc, x1.y *= sc;
   const double tau2 = (g.nugget && g.part == BGP_PART_COV) ? g.p[g.np - 1] : 0.0;
   const double2* cp = reinterpret_cast<const double2*>(colpts);
   double2* dst = reinterpret_cast<double2*>(tile + r);
@@ -183,8 +198,8 @@ __device__ __forceinline__ void cov_tile_fast(const GenDev& g, const double* __r
     const double ax = x0.x - pc.x, ay = x0.y - pc.y;
     const double bx = x1.x - pc.x, by = x1.y - pc.y;
     double2 v;
-    v.x = cov_fast<KIND>(fma(ax, ax, ay * ay), sc, tab);
-    v.y = cov_fast<KIND>(fma(bx, bx, by * by), sc, tab);
+    v.x = cov_fast<KIND>(fma(ax, ax, ay * ay), tab);
+    v.y = cov_fast<KIND>(fma(bx, bx, by * by), tab);
     if (DIAG) {  // rows r, r+1 of a diagonal tile: lower part, nugget where i == j
       v.x = c > r ? 0.0 : (c == r ? v.x + tau2 : v.x);
       v.y = c > r + 1 ? 0.0 : (c == r + 1 ? v.y + tau2 : v.y);
@@ -201,12 +216,12 @@ __device__ __forceinline__ void cov_tile_fast(const GenDev& g, const double* __r
 // triangular: one CTA per lower tile (flat packed index, or an explicit
 // (I, J) list for a rank's share of a 2-D block-cyclic distribution)
 template <bool kPts, int KIND>
-__global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const double* __restrict__ X,
+__global__ void __launch_bounds__(kCovThreads, COV_MIN_BLOCKS) cov_tri_kernel(GenDev g, const double* __restrict__ X,
                                                               int64_t n, int T, int b,
                                                               double* __restrict__ out,
                                                               const int32_t* __restrict__ tile_ij) {
-  extern __shared__ __align__(16) double colpts[];  // b * dim
-  __shared__ double tab[64];          // fast path: sigma^2 2^(j/64)
+  extern __shared__ __align__(16) double colpts[];  // b * dim (fast path: scaled by cov_scale)
+  __shared__ double tab[kExpTab];     // fast path: sigma^2 2^(j/256)
   int I, J;
   if (tile_ij) {
     I = tile_ij[2 * blockIdx.x];
@@ -217,16 +232,18 @@ __global__ void __launch_bounds__(kCovThreads) cov_tri_kernel(GenDev g, const do
   BGP_CHECK(J >= 0 && J <= I && I < T && 2 * b >= blockDim.x);
   const int dim = g.dim;
   const int64_t j0 = (int64_t)J * b, i0 = (int64_t)I * b;
+  const double sc = cov_scale<KIND>(g);  // 1 on the generic path
   for (int t = threadIdx.x; t < b * dim; t += blockDim.x) {
     int64_t jj = j0 + t / dim;
-    colpts[t] = (kPts && jj < n) ? X[jj * dim + t % dim] : 0.0;
+    colpts[t] = (kPts && jj < n) ? X[jj * dim + t % dim] * sc : 0.0;
   }
   // interior tiles (no padding, off the diagonal): no per-entry checks
   // every tile of a 2-D built-in kernel takes the fast path (cov_tile_fast);
   // diagonal tiles mask their strict upper triangle and add the nugget,
   // tiles of the last tile row mask the identity padding
   const bool fast = KIND != 0;
-  if (fast && threadIdx.x < 64) tab[threadIdx.x] = g.p[0] * kExp2Tab[threadIdx.x];
+  if (fast)
+    for (int t = threadIdx.x; t < kExpTab; t += blockDim.x) tab[t] = g.p[0] * kExp2Tab[t];
   __syncthreads();
   double* tile = out + (int64_t)blockIdx.x * b * b;
   if (fast) {
@@ -316,8 +333,8 @@ static int cov_kind(const GenDev& g) {
 static void init_exp_table() {
   static bool done = false;
   if (done) return;
-  double tab[64];
-  for (int j = 0; j < 64; ++j) tab[j] = (double)exp2l((long double)j / 64.0L);
+  double tab[kExpTab];
+  for (int j = 0; j < kExpTab; ++j) tab[j] = (double)exp2l((long double)j / (long double)kExpTab);
   cudaMemcpyToSymbol(kExp2Tab, tab, sizeof(tab));
   done = true;
 }
