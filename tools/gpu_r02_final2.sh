@@ -1,6 +1,6 @@
 # round 2 final measurement pass on the final code (summaries -> profiles/r02final_*)
 set -x
-O=gpurun_out/r02final
+O=${1:-gpurun_out/r02final}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/nvsmi.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt
