@@ -321,10 +321,38 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
   };
 
   *m_first = mk.mark(s);
-  if ((rc = launch_tile_potrf(ctx, tiles, b, row_base, ctx->d_dinv, s, nullptr, 0, T > 1 ? ctx->d_linv : nullptr)))
-    return rc;
-  *m_p0_out = mk.mark(s);
-  if ((rc = panel_solve(0))) return rc;
+  if (T > 1 && trsm_subst && la_mode == 1 && T - 1 <= k_par) {
+    // small problem: POTRF(0) on the role CTA of the panel-0 solve launch,
+    // whose slabs follow it by substitution (no tile inverse, one launch)
+    int* g0 = ctx->d_gate;  // step 0's gate block: [T+1] ticket, [T+2] progress, queue at [stride-2]
+    GemmProblem p{};
+    p.mode = GEMM_TRSM_PANEL;
+    p.b = b;
+    p.T = T;
+    p.J = 0;
+    p.count = T - 1;
+    p.panel0 = tri_index(1, 0, T);
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    p.check_info = true;
+    p.trsm_subst = 1;
+    p.potrf_tile = tiles;
+    p.potrf_row0 = row_base;
+    p.dinv = ctx->d_dinv;
+    p.potrf_progress = g0 + T + 2;
+    p.role_ticket = g0 + T + 1;
+    p.queue = g0 + stride - 2;
+    if ((rc = launch_gemm(ctx, p, tiles, tiles, ntiles, tiles, ntiles, ntiles, s, ctx->d_linv))) return rc;
+    *m_p0_out = mk.mark(s);
+    // the gate block is reused by step 0's launch: zero it again (stream order)
+    cudaError_t e = cudaMemsetAsync(g0, 0, (size_t)stride * sizeof(int), s);
+    if (e != cudaSuccess) return set_err(ctx, "look-ahead counters", e);
+  } else {
+    if ((rc = launch_tile_potrf(ctx, tiles, b, row_base, ctx->d_dinv, s, nullptr, 0, T > 1 ? ctx->d_linv : nullptr)))
+      return rc;
+    *m_p0_out = mk.mark(s);
+    if ((rc = panel_solve(0))) return rc;
+  }
   *m_t0_out = mk.mark(s);
   const int J_last = J_stop < T ? J_stop : T - 1;  // updates with panels 0 .. J_last-1
   for (int J = 0; J < J_last; ++J) {

@@ -312,7 +312,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
                            : p.mode == GEMM_RECT_TRAIL                       ? (int64_t)(p.J + 1) * p.Tm
                                                                              : tri_index(p.J + 2, p.J + 1, p.T);
     trsm_block(it, p, idx, pass, panel0);
-    it.subst = (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST) && p.trsm_subst;
+    it.subst = (p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST || p.mode == GEMM_TRSM_PANEL) && p.trsm_subst;
     // Cholesky sweep: slabs of the last tile row that lie wholly in the
     // padding hold zeros and solve to zeros -- skipped
     if (p.mode == GEMM_CHOL_TRAIL && p.n_live > 0 &&
@@ -395,7 +395,7 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
 __device__ __forceinline__ int gemm_task_passes(const GemmProblem& p, int64_t task) {
   int64_t idx;
   return (gemm_task_kind(p, task, idx) && !(p.mode == GEMM_TRSM_PANEL && p.trsm_oop) && !gemm_par_passes(p) &&
-          !((p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST) && p.trsm_subst))
+          !((p.mode == GEMM_CHOL_TRAIL || p.mode == GEMM_LIST || p.mode == GEMM_TRSM_PANEL) && p.trsm_subst))
              ? p.b / BN
              : 1;
 }
@@ -1101,7 +1101,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else if (ctid < 256) {
         double* psm = reinterpret_cast<double*>(smem);
-        if (ctid == 0) s_go = wait_count(p.col_gate, p.diag_need, info) ? 1 : 0;
+        // (no gate: the first panel's POTRF, fused with its substitution solve)
+        if (ctid == 0) s_go = p.col_gate ? (wait_count(p.col_gate, p.diag_need, info) ? 1 : 0) : 1;
         named_bar_sync(2, 256);
         const bool la_ok = s_go && tile_potrf_inv_device(p.potrf_tile, p.b, p.potrf_row0, p.dinv, info,
                                                         (p.trsm_next && !p.trsm_subst) ? p.linv : nullptr,
