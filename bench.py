@@ -55,6 +55,30 @@ REF_SUB_BLOCKS = 20  # reference sampler: sub-evaluation of 20 reference blocks 
 GEMM_NCU_CAPTURE = "profiles/r02final3_ncu_gemm_full.txt"
 
 
+def hbm_kernels():
+    """The HBM-bound kernels of a C4 step from the committed ncu captures
+    (same pass as GEMM_NCU_CAPTURE): achieved GB/s of algorithmic bytes
+    against the measured HBM copy bandwidth (MEASURED_PEAKS.json)."""
+    import re
+    peak = None
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        peak = 6549.1  # the pool's measured copy bandwidth (round-2 MEASURED_PEAKS.json)
+    out = {}
+    for name, suffix in (("cov_tri_kernel (K1, covariance build)", "ncu_cov_full.txt"),
+                         ("trsv_fwd_persistent_kernel (K3a, forward solve)", "ncu_trsv_full.txt")):
+        path = os.path.join(ROOT, GEMM_NCU_CAPTURE.replace("ncu_gemm_full.txt", suffix))
+        if not os.path.exists(path):
+            continue
+        m = re.search(r"achieved ([0-9.]+) GB/s", open(path).read())
+        if m:
+            gbs = float(m.group(1))
+            out[name] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "source": os.path.relpath(path, ROOT)}
+    return out
+
+
 def gemm_traffic():
     """DRAM bytes (read + write) of one trailing-update launch from the
     committed ncu --set full capture (profiles/*_ncu_gemm_full.txt), with the
@@ -411,7 +435,8 @@ def run_b200(args, world, rank):
                          "algorithmic_flops_per_eval": gemm_flops / facts,
                          "executed_flops_per_eval": executed_flops if world == 1 else None,
                          "launches_per_eval": gemm_launches / facts,
-                         "cublas_dgemm_tflops": CUBLAS_DGEMM},
+                         "cublas_dgemm_tflops": CUBLAS_DGEMM,
+                         "hbm_kernels": hbm_kernels()},
             "parity": parity,
             "clocks": clk,
             "gpu_launches": launches,
