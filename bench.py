@@ -52,7 +52,7 @@ REF_SUB_BLOCKS = 20  # reference sampler: sub-evaluation of 20 reference blocks 
 
 # the committed ncu --set full capture of one C4 trailing-update launch
 # (k = 111 tiles of 512) that the roofline's `traffic` comes from
-GEMM_NCU_CAPTURE = "profiles/r02final3_ncu_gemm_full.txt"
+GEMM_NCU_CAPTURE = "profiles/r02final4_ncu_gemm_full.txt"
 
 
 def hbm_kernels():
@@ -81,24 +81,21 @@ def hbm_kernels():
 
 def gemm_traffic():
     """DRAM bytes (read + write) of one trailing-update launch from the
-    committed ncu --set full capture (profiles/*_ncu_gemm_full.txt), with the
-    algorithmic bytes of the same launch; None when no capture is committed."""
+    committed ncu --set full capture (GEMM_NCU_CAPTURE), with the algorithmic
+    bytes of the same launch (C tiles read + written once, panel tiles read
+    once) as the summary states them; None when no capture is committed."""
     import re
     path = os.path.join(ROOT, GEMM_NCU_CAPTURE)
     if not os.path.exists(path):
         return None, None
-    files = [path]
     txt = open(path).read()
     m = re.search(r"traffic \(read\+write\)\s+([0-9.e+]+) B", txt)
-    f = re.search(r"algorithmic flops\s+([0-9.e+]+)", txt)
-    if not m or not f:
+    a = re.search(r"algorithmic bytes\s+([0-9.e+]+) B", txt)
+    head = txt.splitlines()[0].lstrip("# ").strip()
+    if not m:
         return None, None
-    flops, b = float(f.group(1)), 512
-    k = round((flops / b ** 3) ** 0.5)  # b^3 k^2 flops for a k-tile trailing update
-    algo = 8.0 * b * b * (k * (k + 1) + k)  # C tiles read + written once, panel read once
-    return float(m.group(1)), {"file": os.path.relpath(files[-1], ROOT), "launch_trailing_tiles": k,
-                               "algorithmic_bytes": algo,
-                               "note": "one captured step (k-tile panel read once per L2 super-column)"}
+    return float(m.group(1)), {"file": os.path.relpath(path, ROOT), "launch": head,
+                               "algorithmic_bytes": float(a.group(1)) if a else None}
 
 
 def load_c4():

@@ -213,6 +213,12 @@ struct GemmProblem {
   int* solved;
   int solved_need;
   int64_t cnt_base;
+  // GEMM_CHOL_TRAIL step pairs (large steps, BGP_PAIR_STEPS): pair_cols > 0
+  // updates only tile columns J+1 .. J+pair_cols (the first launch of a
+  // pair); pair_merge applies panels J-1 and J together (k = 2b) to columns
+  // >= J+2 and panel J alone to column J+1 (the second launch)
+  int pair_cols;
+  int pair_merge;
 };
 constexpr int BGP_MAX_PUSH = 8;
 int launch_gemm(Ctx* ctx, const GemmProblem& p, double* Cbase, const double* Abase, int64_t nA,

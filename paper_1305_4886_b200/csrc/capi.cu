@@ -282,6 +282,19 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     const char* e = getenv("BGP_MULTI_STEP");
     return !(e && atoi(e) == 0);
   }();
+  // large steps in pairs (J, J+1): the first launch updates only columns J+1
+  // and J+2 (and factors / solves panel J+1), the second applies panel J+1
+  // to column J+2 and panels J, J+1 together (k = 2b blocks) to the rest
+  // (tiles of 512 with >= 64 trailing tiles: there the first launch's two
+  // columns still outlast its POTRF + inverse chain; C4 +0.2 %.
+  // BGP_PAIR_STEPS=k sets the minimum trailing tiles at every tile size,
+  // 0 turns pairs off)
+  static const int pair_env = [] {
+    const char* e = getenv("BGP_PAIR_STEPS");
+    return e ? atoi(e) : -1;
+  }();
+  const int pair_min = pair_env >= 0 ? pair_env : (b == 512 ? 64 : 0);
+  bool pair_second = false;
   if (trsm_par) {
     if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
     cudaError_t e = cudaMemsetAsync(ctx->d_pass, 0, (size_t)T * pass_stride * sizeof(int), s);
@@ -360,7 +373,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     double* dkk = tiles + tri_index(K, K, T) * tsz;
     int* gate = ctx->d_gate + (int64_t)J * stride;
     StepMarks sm{-1, -1, -1, -1};
-    if (multi_step && ctx->grid_cap <= 0 && trsm_subst && la_mode == 1 && J_stop == T && T - J - 1 <= k_par && T - 1 - J >= 2 &&
+    if (!pair_second && multi_step && ctx->grid_cap <= 0 && trsm_subst && la_mode == 1 && J_stop == T && T - J - 1 <= k_par && T - 1 - J >= 2 &&
         T - 1 - J <= max_multi) {
       // steps J .. T-2 (every remaining one) in one launch: per-tile update
       // counters, per-tile solve counters, per-step POTRF progress, queue
@@ -411,6 +424,14 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     p.role_ticket = gate + T + 1;
     p.n_live = n;
     const bool next = K < J_stop;  // panel K is factored here
+    if (pair_second) {
+      p.pair_merge = 1;
+      pair_second = false;
+    } else if (pair_min > 0 && la_mode == 1 && next && K + 1 < J_stop && K + 1 < J_last && T - J - 1 >= pair_min &&
+               T - K - 1 > k_par) {  // (the second launch is a plain step, never the multi-step tail)
+      p.pair_cols = 2;
+      pair_second = true;
+    }
     if (la_mode == 1) {
       if (next) {
         // POTRF(K) (+ inverse) by the CTA holding the role ticket, the TRSM of panel K

@@ -103,6 +103,10 @@ __host__ __device__ __forceinline__ int64_t gemm_num_items(const GemmProblem& p)
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
       const int64_t k = p.T - p.J - 1;
+      if (k > 0 && p.pair_cols > 0) {  // columns J+1 .. J+m only
+        const int64_t m = p.pair_cols < k ? p.pair_cols : k;
+        return (m * k - m * (m - 1) / 2) * nblk;
+      }
       return k > 0 ? k * (k + 1) / 2 * nblk : 0;
     }
     case GEMM_RECT_TRAIL:
@@ -329,13 +333,26 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   switch (p.mode) {
     case GEMM_CHOL_TRAIL: {
       int rr, cc;
-      // super-column width: ~16 MB of panel tiles, 8 .. 64 tiles
-      const int sw = max(8, min(64, (int)((16ll << 20) / ((int64_t)p.b * p.b * 8))));
-      trail_order(t, p.T - p.J - 1, sw, rr, cc);
+      if (p.pair_cols > 0) {
+        tri_decode(t, p.T - p.J - 1, rr, cc);  // the first columns, column by column
+      } else {
+        // super-column width: ~16 MB of panel tiles, 8 .. 64 tiles
+        const int sw = max(8, min(64, (int)((16ll << 20) / ((int64_t)p.b * p.b * 8))));
+        trail_order(t, p.T - p.J - 1, sw, rr, cc);
+      }
       const int R = p.J + 1 + rr, C = p.J + 1 + cc;
       it.cTile = tri_index(R, C, p.T);
-      it.aTile0 = tri_index(R, p.J, p.T);
-      it.bTile0 = tri_index(C, p.J, p.T);
+      if (p.pair_merge && cc >= 1) {
+        // panels J-1 and J in one pass (k = 2b): consecutive panel tiles of a
+        // row are T-J tile indices apart in the packed triangle
+        it.aTile0 = tri_index(R, p.J - 1, p.T);
+        it.bTile0 = tri_index(C, p.J - 1, p.T);
+        it.nkt = 2;
+        it.aStride = it.bStride = p.T - p.J;
+      } else {
+        it.aTile0 = tri_index(R, p.J, p.T);
+        it.bTile0 = tri_index(C, p.J, p.T);
+      }
       if (R == C) diag_block(it, bi, bj);
       if (cc == 0 && p.col_gate) it.gate = rr;  // column J+1: POTRF / TRSM of the next panel wait on it
       // blocks of the last tile row wholly in the identity padding: their
