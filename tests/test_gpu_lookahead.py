@@ -183,3 +183,35 @@ def test_one_launch_per_step_fallback_matches(tmp_path):
     want = np.linalg.cholesky(spd_matrix(n, seed=2))
     assert relerr(out["0"], want) <= 1e-12 and relerr(out["1"], want) <= 1e-12
     assert relerr(out["0"], out["1"]) <= 1e-13
+
+
+@pytest.mark.parametrize("tile,ntiles", [(128, 56), (256, 31)])
+def test_step_pairs_forced_match_lapack(tmp_path, tile, ntiles):
+    """Step pairs (the second launch applies two panels at once, 2b-deep
+    blocks; by default only from 64 trailing tiles at tile 512) forced with
+    BGP_PAIR_STEPS=2 (read once per process, so in a subprocess): pairs then
+    run wherever the second step is not chain-bound (more than 48 / 26
+    trailing tiles at 128 / 256).  The factor and the log-determinant
+    against LAPACK."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = tile * ntiles - 29
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from conftest import spd_matrix\n"
+        "from paper_1305_4886_b200 import distla, spawn\n"
+        "cl = spawn(1, tile=%d); n = %d; A = spd_matrix(n, seed=n)\n"
+        "C = distla.distribute(cl, 'C', A, 'triangular', distla.make_layout(n, cl.grid, h=3))\n"
+        "L, _ = distla.distributed_cholesky(cl, C, 'L')\n"
+        "np.save(sys.argv[1], distla.collect(cl, L)); np.save(sys.argv[2], distla.log_det_from_chol(cl, L))\n"
+        "cl.shutdown()\n") % (root, os.path.join(root, "tests"), tile, n)
+    fL, fd = str(tmp_path / "L.npy"), str(tmp_path / "d.npy")
+    env = dict(os.environ, BGP_PAIR_STEPS="2")
+    subprocess.run([sys.executable, "-c", code, fL, fd], check=True, env=env, timeout=900)
+    A = spd_matrix(n, seed=n)
+    want = np.linalg.cholesky(A)
+    assert relerr(np.load(fL), want) <= 1e-12
+    ld = float(np.load(fd))
+    assert abs(ld - np.linalg.slogdet(A)[1]) <= 1e-10 * abs(np.linalg.slogdet(A)[1])
