@@ -215,3 +215,31 @@ def test_step_pairs_forced_match_lapack(tmp_path, tile, ntiles):
     assert relerr(np.load(fL), want) <= 1e-12
     ld = float(np.load(fd))
     assert abs(ld - np.linalg.slogdet(A)[1]) <= 1e-10 * abs(np.linalg.slogdet(A)[1])
+
+
+def test_step_pairs_forced_failure(tmp_path):
+    """A non-positive pivot on the diagonal tile a pair's first launch
+    factors (tile 3 of 56 at tile 128, pairs forced): NotPositiveDefinite
+    with the right block, no hang, no factor left behind."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from conftest import spd_matrix\n"
+        "from paper_1305_4886_b200 import distla, spawn\n"
+        "from paper_1305_4886_b200.errors import NotPositiveDefinite\n"
+        "cl = spawn(1, tile=128); n = 128 * 56 - 5; A = spd_matrix(n, seed=5); bad = 3 * 128 + 40\n"
+        "A[bad, bad] = -1.0; lay = distla.make_layout(n, cl.grid, h=8)\n"
+        "C = distla.distribute(cl, 'C', A, 'triangular', lay)\n"
+        "try:\n"
+        "    distla.distributed_cholesky(cl, C, 'L'); print('NO-FAILURE')\n"
+        "except NotPositiveDefinite as e:\n"
+        "    ok = e.block_index == bad // lay.block_size + 1 and 'L' not in set(cl.remote_ls())\n"
+        "    print('OK' if ok else 'WRONG %%d' %% e.block_index)\n"
+        "cl.shutdown()\n") % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, BGP_PAIR_STEPS="2")
+    out = subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=900, capture_output=True,
+                         text=True).stdout
+    assert out.strip().splitlines()[-1] == "OK", out
