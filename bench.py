@@ -52,7 +52,7 @@ REF_SUB_BLOCKS = 20  # reference sampler: sub-evaluation of 20 reference blocks 
 
 # the committed ncu --set full capture of one C4 trailing-update launch
 # (k = 111 tiles of 512) that the roofline's `traffic` comes from
-GEMM_NCU_CAPTURE = "profiles/r02final4_ncu_gemm_full.txt"
+GEMM_NCU_CAPTURE = "profiles/r02final5_ncu_gemm_full.txt"
 
 
 def hbm_kernels():

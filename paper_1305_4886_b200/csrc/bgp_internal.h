@@ -213,10 +213,11 @@ struct GemmProblem {
   int* solved;
   int solved_need;
   int64_t cnt_base;
-  // GEMM_CHOL_TRAIL step pairs (large steps, BGP_PAIR_STEPS): pair_cols > 0
-  // updates only tile columns J+1 .. J+pair_cols (the first launch of a
-  // pair); pair_merge applies panels J-1 and J together (k = 2b) to columns
-  // >= J+2 and panel J alone to column J+1 (the second launch)
+  // GEMM_CHOL_TRAIL step groups (large steps, BGP_PAIR_STEPS; pairs by
+  // default): pair_cols > 0 updates only tile columns J+1 .. J+pair_cols (the
+  // thin launches of a group); pair_merge = m > 0 applies panels J-m .. J
+  // together (k = (m+1) b) to columns >= J+2 and panel J alone to column J+1
+  // (the group's last launch)
   int pair_cols;
   int pair_merge;
 };

@@ -282,19 +282,25 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     const char* e = getenv("BGP_MULTI_STEP");
     return !(e && atoi(e) == 0);
   }();
-  // large steps in pairs (J, J+1): the first launch updates only columns J+1
-  // and J+2 (and factors / solves panel J+1), the second applies panel J+1
-  // to column J+2 and panels J, J+1 together (k = 2b blocks) to the rest
-  // (tiles of 512 with >= 64 trailing tiles: there the first launch's two
-  // columns still outlast its POTRF + inverse chain; C4 +0.2 %.
-  // BGP_PAIR_STEPS=k sets the minimum trailing tiles at every tile size,
-  // 0 turns pairs off)
+  // large steps in groups of d (default 5): launch i < d updates only
+  // columns J+i .. J+d with panel J+i-1 (and factors / solves panel J+i as
+  // usual), the group's last launch applies panel J+d-1 to column J+d and
+  // panels J .. J+d-1 together (k = d b blocks) to every other column.
+  // Tiles of 512 with >= 64 trailing tiles: there the thin launches still
+  // outlast their POTRF + inverse chain (C4 +0.5 %, profiles/r02grp*).
+  // BGP_PAIR_STEPS=k sets the minimum trailing tiles at every tile size
+  // (0: off), BGP_GROUP_DEPTH=d the group size (2 .. 6).
   static const int pair_env = [] {
     const char* e = getenv("BGP_PAIR_STEPS");
     return e ? atoi(e) : -1;
   }();
   const int pair_min = pair_env >= 0 ? pair_env : (b == 512 ? 64 : 0);
-  bool pair_second = false;
+  static const int group_depth = [] {
+    const char* e = getenv("BGP_GROUP_DEPTH");
+    const int d = e ? atoi(e) : 5;
+    return d < 2 ? 2 : (d > 6 ? 6 : d);
+  }();
+  int group_left = 0;  // launches of the current group still to come
   if (trsm_par) {
     if ((rc = ensure(ctx, (void**)&ctx->d_pass, &ctx->pass_cap, (size_t)T * pass_stride * sizeof(int)))) return rc;
     cudaError_t e = cudaMemsetAsync(ctx->d_pass, 0, (size_t)T * pass_stride * sizeof(int), s);
@@ -373,7 +379,7 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     double* dkk = tiles + tri_index(K, K, T) * tsz;
     int* gate = ctx->d_gate + (int64_t)J * stride;
     StepMarks sm{-1, -1, -1, -1};
-    if (!pair_second && multi_step && ctx->grid_cap <= 0 && trsm_subst && la_mode == 1 && J_stop == T && T - J - 1 <= k_par && T - 1 - J >= 2 &&
+    if (group_left == 0 && multi_step && ctx->grid_cap <= 0 && trsm_subst && la_mode == 1 && J_stop == T && T - J - 1 <= k_par && T - 1 - J >= 2 &&
         T - 1 - J <= max_multi) {
       // steps J .. T-2 (every remaining one) in one launch: per-tile update
       // counters, per-tile solve counters, per-step POTRF progress, queue
@@ -424,13 +430,18 @@ static int potrf_run(Ctx* ctx, double* tiles, int64_t n, int b, cudaStream_t s, 
     p.role_ticket = gate + T + 1;
     p.n_live = n;
     const bool next = K < J_stop;  // panel K is factored here
-    if (pair_second) {
-      p.pair_merge = 1;
-      pair_second = false;
-    } else if (pair_min > 0 && la_mode == 1 && next && K + 1 < J_stop && K + 1 < J_last && T - J - 1 >= pair_min &&
-               T - K - 1 > k_par) {  // (the second launch is a plain step, never the multi-step tail)
-      p.pair_cols = 2;
-      pair_second = true;
+    const int d = group_depth;
+    if (group_left > 1) {  // a thin launch inside the group
+      p.pair_cols = group_left;
+      --group_left;
+    } else if (group_left == 1) {  // the group's last launch: d panels merged
+      p.pair_merge = d - 1;
+      group_left = 0;
+    } else if (pair_min > 0 && la_mode == 1 && next && J + d < J_stop && J + d - 1 < J_last &&
+               T - J - 1 >= pair_min &&
+               T - (J + d - 1) - 1 > k_par) {  // (its launches are plain steps, never the multi-step tail)
+      p.pair_cols = d;
+      group_left = d - 1;
     }
     if (la_mode == 1) {
       if (next) {

@@ -83,7 +83,9 @@ static_assert((GROUPS * 2 * STAGES + 1) * 8 <= 256 && 256 + GROUPS * STAGES * 48
 
 struct Item {
   int cTile, aTile0, bTile0;  // tile indices (< 2^31: 1.4e5 tiles at n = 131,072, b = 256)
-  int bTriRow;               // >= 0: B tile for k tile kt is L(bTriRow, kt) (TRMM)
+  int bTriRow;               // >= 0: B tile for k tile kt is L(bTriRow, triCol0 + kt) (TRMM, merged panels)
+  int aTriRow;               // >= 0: A tile for k tile kt is L(aTriRow, triCol0 + kt) (merged panels)
+  int triCol0;
   int aStride, bStride;      // tile-index stride per k tile
   int nkt;                   // number of k tiles
   int mrow0, nrow0;          // row offsets inside the A / B tiles (= C block offsets)
@@ -295,6 +297,8 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
   it.subst = false;
   it.lower = 0;
   it.bTriRow = -1;
+  it.aTriRow = -1;
+  it.triCol0 = 0;
   it.kstages = 0;
   it.store = (p.beta == 0.0);
   it.bLinv = 0;
@@ -336,19 +340,24 @@ __device__ __forceinline__ Item gemm_decode(const GemmProblem& p, int64_t task, 
       if (p.pair_cols > 0) {
         tri_decode(t, p.T - p.J - 1, rr, cc);  // the first columns, column by column
       } else {
-        // super-column width: ~16 MB of panel tiles, 8 .. 64 tiles
-        const int sw = max(8, min(64, (int)((16ll << 20) / ((int64_t)p.b * p.b * 8))));
+        // super-column width: ~16 MB of panel tiles per merged panel depth
+        // (8 .. 64 tiles; 2 .. 64 when several panels are merged)
+        const int depth = p.pair_merge + 1;
+        const int sw = max(depth > 1 ? 2 : 8, min(64, (int)((16ll << 20) / ((int64_t)depth * p.b * p.b * 8))));
         trail_order(t, p.T - p.J - 1, sw, rr, cc);
       }
       const int R = p.J + 1 + rr, C = p.J + 1 + cc;
       it.cTile = tri_index(R, C, p.T);
       if (p.pair_merge && cc >= 1) {
-        // panels J-1 and J in one pass (k = 2b): consecutive panel tiles of a
-        // row are T-J tile indices apart in the packed triangle
-        it.aTile0 = tri_index(R, p.J - 1, p.T);
-        it.bTile0 = tri_index(C, p.J - 1, p.T);
-        it.nkt = 2;
-        it.aStride = it.bStride = p.T - p.J;
+        // panels J-m .. J in one pass (k = (m+1) b); the k tile kt of a row
+        // is its tile in panel J-m+kt (tri_index per k tile: the packed
+        // triangle's column starts are not equally spaced)
+        it.aTile0 = tri_index(R, p.J - p.pair_merge, p.T);
+        it.bTile0 = tri_index(C, p.J - p.pair_merge, p.T);
+        it.nkt = p.pair_merge + 1;
+        it.aTriRow = R;
+        it.bTriRow = C;
+        it.triCol0 = p.J - p.pair_merge;
       } else {
         it.aTile0 = tri_index(R, p.J, p.T);
         it.bTile0 = tri_index(C, p.J, p.T);
@@ -588,43 +597,47 @@ __device__ __forceinline__ void producer_loop(const GroupSmem& gs, const CUtenso
       const CUtensorMap* tb = it.bLinv ? tmL : tmB;
       const CUtensorMap* ta = (it.bLinv && !p.trsm_oop) ? tmT : tmA;
       const int nk = it.kstages > 0 ? it.kstages : it.nkt * kc_per_tile;
-      for (int kc = 0; kc < nk; ++kc) {
-        mbar_wait(&gs.empty[stage], phase ^ 1);
-        if (kc == 0) {  // read by the consumers after `full`
-          BlockSlot& sl = gs.slot[stage];
-          sl.valid = 1;
-          sl.cTile = it.cTile;
-          sl.mrow0 = it.mrow0;
-          sl.nrow0 = it.nrow0;
-          sl.nk = nk;
-          sl.lower = it.lower;
-          sl.store = it.store;
-          sl.gate = it.gate;
-          sl.slab = it.slab;
-          sl.pass = it.pass;
-          sl.pad[0] = 0;
-        }
-        mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
-        const int kt = kc / kc_per_tile;
-        const int kin = (kc % kc_per_tile) * BK;
-        const int at = (int)(it.aTile0 + kt * it.aStride);
-        const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, kt, q.T)
+      // k tiles outer (their tile indices computed once per k tile), BK
+      // stages inner
+      int kc = 0;
+      for (int kt = 0; kc < nk; ++kt) {
+        const int at = it.aTriRow >= 0 ? (int)tri_index(it.aTriRow, it.triCol0 + kt, q.T)
+                                       : (int)(it.aTile0 + kt * it.aStride);
+        const int bt = it.bTriRow >= 0 ? (int)tri_index(it.bTriRow, it.triCol0 + kt, q.T)
                                        : (int)(it.bTile0 + kt * it.bStride);
         BGP_CHECK(at >= 0 && at < (ta == tmT ? p.nC : p.nA));
         BGP_CHECK(bt >= 0 && bt < (it.bLinv ? 1 : p.nB));
         BGP_CHECK(it.mrow0 >= 0 && it.mrow0 + BM <= p.b && it.nrow0 >= 0 && it.nrow0 + BN <= p.b);
-        BGP_CHECK(kin + BK <= p.b);
-        uint8_t* sa = gs.stages + stage * STAGE_BYTES;
-        uint8_t* sb = sa + STAGE_A_BYTES;
+        for (int kin = 0; kin < p.b && kc < nk; kin += BK, ++kc) {
+          mbar_wait(&gs.empty[stage], phase ^ 1);
+          if (kc == 0) {  // read by the consumers after `full`
+            BlockSlot& sl = gs.slot[stage];
+            sl.valid = 1;
+            sl.cTile = it.cTile;
+            sl.mrow0 = it.mrow0;
+            sl.nrow0 = it.nrow0;
+            sl.nk = nk;
+            sl.lower = it.lower;
+            sl.store = it.store;
+            sl.gate = it.gate;
+            sl.slab = it.slab;
+            sl.pass = it.pass;
+            sl.pad[0] = 0;
+          }
+          mbar_arrive_expect_tx(&gs.full[stage], STAGE_BYTES);
+          BGP_CHECK(kin + BK <= p.b);
+          uint8_t* sa = gs.stages + stage * STAGE_BYTES;
+          uint8_t* sb = sa + STAGE_A_BYTES;
 #pragma unroll
-        for (int i = 0; i < BM / 16; ++i)
-          tma_load_3d(sa + i * BOX_BYTES, ta, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
+          for (int i = 0; i < BM / 16; ++i)
+            tma_load_3d(sa + i * BOX_BYTES, ta, &gs.full[stage], it.mrow0 + i * 16, kin, at, pol_keep);
 #pragma unroll
-        for (int i = 0; i < BN / 16; ++i)
-          tma_load_3d(sb + i * BOX_BYTES, tb, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int i = 0; i < BN / 16; ++i)
+            tma_load_3d(sb + i * BOX_BYTES, tb, &gs.full[stage], it.nrow0 + i * 16, kin, bt, pol_keep);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }

@@ -185,14 +185,14 @@ def test_one_launch_per_step_fallback_matches(tmp_path):
     assert relerr(out["0"], out["1"]) <= 1e-13
 
 
-@pytest.mark.parametrize("tile,ntiles", [(128, 56), (256, 31)])
-def test_step_pairs_forced_match_lapack(tmp_path, tile, ntiles):
-    """Step pairs (the second launch applies two panels at once, 2b-deep
-    blocks; by default only from 64 trailing tiles at tile 512) forced with
-    BGP_PAIR_STEPS=2 (read once per process, so in a subprocess): pairs then
-    run wherever the second step is not chain-bound (more than 48 / 26
-    trailing tiles at 128 / 256).  The factor and the log-determinant
-    against LAPACK."""
+@pytest.mark.parametrize("tile,ntiles,depth", [(128, 56, 2), (128, 60, 5), (256, 33, 3)])
+def test_step_groups_forced_match_lapack(tmp_path, tile, ntiles, depth):
+    """Step groups (the group's last launch applies `depth` panels at once,
+    depth*b-deep blocks; by default groups of 5 from 64 trailing tiles at
+    tile 512) forced with BGP_PAIR_STEPS=2 (read once per process, so in a
+    subprocess): groups then run wherever their last step is not
+    chain-bound (more than 48 / 26 trailing tiles at 128 / 256).  The
+    factor and the log-determinant against LAPACK."""
     import os
     import subprocess
     import sys
@@ -208,7 +208,7 @@ def test_step_pairs_forced_match_lapack(tmp_path, tile, ntiles):
         "np.save(sys.argv[1], distla.collect(cl, L)); np.save(sys.argv[2], distla.log_det_from_chol(cl, L))\n"
         "cl.shutdown()\n") % (root, os.path.join(root, "tests"), tile, n)
     fL, fd = str(tmp_path / "L.npy"), str(tmp_path / "d.npy")
-    env = dict(os.environ, BGP_PAIR_STEPS="2")
+    env = dict(os.environ, BGP_PAIR_STEPS="2", BGP_GROUP_DEPTH=str(depth))
     subprocess.run([sys.executable, "-c", code, fL, fd], check=True, env=env, timeout=900)
     A = spd_matrix(n, seed=n)
     want = np.linalg.cholesky(A)
@@ -217,10 +217,11 @@ def test_step_pairs_forced_match_lapack(tmp_path, tile, ntiles):
     assert abs(ld - np.linalg.slogdet(A)[1]) <= 1e-10 * abs(np.linalg.slogdet(A)[1])
 
 
-def test_step_pairs_forced_failure(tmp_path):
-    """A non-positive pivot on the diagonal tile a pair's first launch
-    factors (tile 3 of 56 at tile 128, pairs forced): NotPositiveDefinite
-    with the right block, no hang, no factor left behind."""
+@pytest.mark.parametrize("depth", [2, 5])
+def test_step_groups_forced_failure(tmp_path, depth):
+    """A non-positive pivot on a diagonal tile factored inside a step group
+    (tile 3 of 56 at tile 128, groups forced): NotPositiveDefinite with the
+    right block, no hang, no factor left behind."""
     import os
     import subprocess
     import sys
@@ -239,7 +240,7 @@ def test_step_pairs_forced_failure(tmp_path):
         "    ok = e.block_index == bad // lay.block_size + 1 and 'L' not in set(cl.remote_ls())\n"
         "    print('OK' if ok else 'WRONG %%d' %% e.block_index)\n"
         "cl.shutdown()\n") % (root, os.path.join(root, "tests"))
-    env = dict(os.environ, BGP_PAIR_STEPS="2")
+    env = dict(os.environ, BGP_PAIR_STEPS="2", BGP_GROUP_DEPTH=str(depth))
     out = subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=900, capture_output=True,
                          text=True).stdout
     assert out.strip().splitlines()[-1] == "OK", out
